@@ -1,0 +1,273 @@
+"""Pins for the oracle (CPU only): the oracle is checked against what the paper and the
+mathematics fix, never against itself (SURVEY.md §8(c) "Pins")."""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests.conftest import GOLDEN
+from tests.exact.arpa_py import ArpaPy
+from tests.exact.boost_py import BoostPy
+from tests.exact.ctc_exact import brute_force, ctc_forward, greedy
+from tests.exact.exhaustive import exhaustive
+
+INF = float("inf")
+
+
+def _rand_logprobs(rng, T, Vp1, scale=1.5):
+    x = rng.standard_normal((T, Vp1)) * scale
+    return x - np.log(np.exp(x).sum(1, keepdims=True))
+
+
+# ---------------------------------------------------------------- worked examples (SPEC)
+
+def test_worked_T2_example(golden):
+    g = golden["decode"]["worked_T2"]
+    D = np.log(np.array(g["D"]))
+    res = oracle.decode_nbest(D, oracle.make_cfg(4))
+    assert res[0][0] == tuple(g["lse"]["best"])
+    assert res[0][1] == pytest.approx(g["lse"]["best_score"], abs=1e-12)
+    assert res[1][0] == tuple(g["lse"]["runner_up"])
+    assert res[1][1] == pytest.approx(g["lse"]["runner_up_score"], abs=1e-12)
+    resm = oracle.decode_nbest(D, oracle.make_cfg(4, merge_mode=1))
+    assert resm[0][0] == tuple(g["max"]["best"])
+    assert resm[0][1] == pytest.approx(g["max"]["best_score"], abs=1e-12)
+
+
+def test_worked_T2_fp32_path(golden):
+    g = golden["decode"]["worked_T2"]
+    D = np.log(np.array(g["D"], dtype=np.float64)).astype(np.float32)[None]
+    out = oracle.decode(D, [2], oracle.make_cfg(4))
+    assert out["num_tokens"][0] == 1 and out["tokens"][0, 0] == 0
+    assert out["scores"][0] == pytest.approx(g["lse"]["best_score"], abs=1e-6)
+
+
+def test_theta_prune_example(golden):
+    g = golden["decode"]["theta_prune"]
+    D = np.array(g["D"])
+    assert len(oracle.decode_nbest(D, oracle.make_cfg(2, theta=g["theta"]))) == g["n_alive"]
+    assert len(oracle.decode_nbest(D, oracle.make_cfg(2, theta=INF))) == 2
+
+
+def test_greedy_example(golden):
+    g = golden["decode"]["greedy_T2"]
+    D = np.log(np.array(golden["decode"]["worked_T2"]["D"]))
+    res = oracle.decode_nbest(D, oracle.make_cfg(1))
+    assert res[0][0] == tuple(g["tokens"])
+    assert res[0][1] == pytest.approx(g["score"], abs=1e-12)
+
+
+# ---------------------------------------------------------------- K = 1 == greedy
+
+def test_beam1_equals_greedy_random():
+    rng = np.random.default_rng(1)
+    for trial in range(200):
+        B = int(rng.integers(1, 9))
+        T = int(rng.integers(1, 51))
+        Vp1 = int(rng.integers(2, 17))
+        D = np.stack([_rand_logprobs(rng, T, Vp1, 2.0) for _ in range(B)]).astype(np.float32)
+        L = rng.integers(1, T + 1, B)
+        out = oracle.decode(D, L, oracle.make_cfg(1), nthreads=2)
+        for b in range(B):
+            toks, score, _ = greedy(D[b, :L[b]], Vp1 - 1)
+            n = out["num_tokens"][b]
+            assert tuple(out["tokens"][b, :n]) == toks, (trial, b)
+            assert out["scores"][b] == np.float32(score), (trial, b)
+
+
+# ---------------------------------------------------------------- exact CTC (brute force, forward, ctc_loss)
+
+@pytest.mark.parametrize("T,Vp1", [(1, 2), (2, 3), (3, 3), (4, 3), (5, 3), (6, 3), (3, 4), (4, 4), (5, 4), (6, 4),
+                                   (3, 5), (4, 5), (5, 5)])
+@pytest.mark.parametrize("mode", ["lse", "max"])
+def test_full_beam_equals_brute_force(T, Vp1, mode):
+    """θ = ∞, no fusion, K = V'^T (>= live states × V' at every frame): every transcript's score
+    is exact (SURVEY §8(c) pin 1)."""
+    rng = np.random.default_rng(100 * T + Vp1)
+    K = Vp1 ** T
+    for _ in range(3):
+        D = _rand_logprobs(rng, T, Vp1)
+        bf = brute_force(D, Vp1 - 1, mode)
+        res = dict(oracle.decode_nbest(D, oracle.make_cfg(K, merge_mode=0 if mode == "lse" else 1)))
+        assert set(res) == set(bf)
+        for y, s in bf.items():
+            assert res[y] == pytest.approx(s, abs=1e-10), y
+
+
+def test_brute_force_equals_ctc_forward_and_ctc_loss():
+    """Pins the brute-force checker itself against the textbook forward algorithm and the
+    library routine torch.nn.functional.ctc_loss (which returns -log P(y|x))."""
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        T, Vp1 = int(rng.integers(1, 6)), int(rng.integers(2, 5))
+        D = _rand_logprobs(rng, T, Vp1)
+        bf = brute_force(D, Vp1 - 1)
+        for y, s in bf.items():
+            assert ctc_forward(D, y, Vp1 - 1) == pytest.approx(s, abs=1e-10)
+            if len(y) == 0:
+                continue
+            lp = torch.tensor(D, dtype=torch.float64)[:, None, :]
+            loss = torch.nn.functional.ctc_loss(lp, torch.tensor([list(y)]), torch.tensor([T]),
+                                                torch.tensor([len(y)]), blank=Vp1 - 1, reduction="none")
+            assert -float(loss[0]) == pytest.approx(s, abs=1e-9)
+
+
+def test_full_beam_matches_ctc_loss_t6():
+    T, Vp1 = 6, 4
+    rng = np.random.default_rng(9)
+    D = _rand_logprobs(rng, T, Vp1)
+    res = oracle.decode_nbest(D, oracle.make_cfg(Vp1 ** T))
+    for y, s in res[:20]:
+        if not y:
+            continue
+        lp = torch.tensor(D)[:, None, :]
+        loss = torch.nn.functional.ctc_loss(lp, torch.tensor([list(y)]), torch.tensor([T]), torch.tensor([len(y)]),
+                                            blank=Vp1 - 1, reduction="none")
+        assert s == pytest.approx(-float(loss[0]), abs=1e-9)
+
+
+# ---------------------------------------------------------------- LM fixtures
+
+@pytest.mark.parametrize("fx,path", [("lm_2gram", "arpa_2gram.arpa"), ("lm_3gram", "arpa_3gram.arpa")])
+def test_lm_fixture_values(golden, fx, path):
+    g = golden[fx]
+    syms = g["symbols"]
+    lm = oracle.LM(os.path.join(GOLDEN, path), len(syms), syms)
+    py = ArpaPy(os.path.join(GOLDEN, path))
+    idx = {s: i for i, s in enumerate(syms)}
+    for e in g["logp"]:
+        hist = [idx[s] for s in e["hist"]]
+        w = -1 if e["w"] == "</s>" else idx[e["w"]]
+        assert lm.logp(hist, w) == pytest.approx(e["value"], abs=1e-7), e
+        assert lm.logp(hist, w, f32=True) == pytest.approx(e["value"], abs=2e-6), e
+        assert py.logp(["<s>"] + e["hist"], e["w"]) == pytest.approx(e["value"], abs=1e-7), e
+    for e in g["seq"]:
+        assert lm.seq([idx[s] for s in e["tokens"]]) == pytest.approx(e["value"], abs=1e-7), e
+        assert py.seq(e["tokens"]) == pytest.approx(e["value"], abs=1e-7), e
+
+
+def test_lm_errors(tmp_path):
+    p = tmp_path / "bad.arpa"
+    p.write_text("\\data\\\nngram 1=2\n\n\\1-grams:\n-1.0\t</s>\n\\end\\\n")
+    with pytest.raises(ValueError, match="count mismatch"):
+        oracle.LM(str(p), 1)
+    p.write_text("\\data\\\nngram 1=1\n\n\\1-grams:\n-1.0\ta\n\\end\\\n")
+    with pytest.raises(ValueError, match="</s>"):
+        oracle.LM(str(p), 1, ["a"])
+    p.write_text("\\data\\\nngram 1=1\n\n\\1-grams:\n-1.0\t</s>\n")
+    with pytest.raises(ValueError, match="end"):
+        oracle.LM(str(p), 1)
+    p.write_text("\\data\\\nngram 1=2\n\n\\1-grams:\n-1.0\t</s>\n-1.0\ta\n\\end\\\n")
+    with pytest.raises(ValueError, match="not in LM"):
+        oracle.LM(str(p), 2, ["a", "zz"])
+
+
+# ---------------------------------------------------------------- boosting fixtures
+
+def test_boost_fixture_values(golden):
+    g = golden["boost"]
+    for e in g["cases"]:
+        bt = oracle.Boost(e["phrases"], e["w"], 16)
+        assert bt.delta(e["prefix"], e["token"]) == pytest.approx(e["delta"], abs=1e-12), e
+        assert bt.delta(e["prefix"], e["token"], f32=True) == e["delta"], e
+        py = BoostPy(e["phrases"], e["w"])
+        u = 0
+        for a in e["prefix"]:
+            u = py.step(u, a)
+        assert py.delta(u, e["token"])[0] == pytest.approx(e["delta"], abs=1e-12), e
+    for e in g["U"]:
+        assert oracle.Boost(e["phrases"], e["w"], 16).U(e["prefix"]) == pytest.approx(e["U"]), e
+    for e in g["transition_depth"]:
+        assert oracle.Boost(e["phrases"], 1.0, 16).state_depth(e["prefix"]) == e["depth"], e
+    for e in g["sums"]:
+        bt = oracle.Boost(e["phrases"], e["w"], 16)
+        tot = sum(bt.delta(e["stream"][:i], e["stream"][i]) for i in range(len(e["stream"])))
+        assert tot == pytest.approx(e["total"], abs=1e-12), e
+        assert BoostPy(e["phrases"], e["w"]).total(e["stream"])[0] == pytest.approx(e["total"], abs=1e-12), e
+
+
+def test_boost_naive_equals_aho_corasick_random():
+    """Naive longest-suffix matching (oracle) == Aho-Corasick transition (tests/exact)."""
+    rng = np.random.default_rng(3)
+    for trial in range(60):
+        V = int(rng.integers(2, 7))
+        n = int(rng.integers(1, 8))
+        phrases = [list(rng.integers(0, V, int(rng.integers(1, 5)))) for _ in range(n)]
+        w = float(rng.uniform(0.2, 2.0))
+        bt = oracle.Boost(phrases, w, V)
+        py = BoostPy(phrases, w)
+        stream = list(rng.integers(0, V, 40))
+        u, tel = 0, 0.0
+        for i, a in enumerate(stream):
+            d_py, v = py.delta(u, int(a))
+            assert bt.delta(stream[:i], int(a)) == pytest.approx(d_py, abs=1e-12)
+            assert bt.state_depth(stream[:i + 1]) == py.depth[v]
+            assert bt.U(stream[:i + 1]) == pytest.approx(py.U[v], abs=1e-12)
+            tel += d_py
+            u = v
+        # telescoping: Σ deltas = committed total + U(end)  => Σ - U(end) = committed >= 0
+        assert tel - py.U[u] >= -1e-9
+
+
+def test_boost_errors():
+    with pytest.raises(ValueError):
+        oracle.Boost([], 1.0, 4)
+    with pytest.raises(ValueError):
+        oracle.Boost([[]], 1.0, 4)
+    with pytest.raises(ValueError):
+        oracle.Boost([[1, 4]], 1.0, 4)  # 4 == blank for V=4
+
+
+# ---------------------------------------------------------------- Eq. (1) exactness with LM, BT, β
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("retract", [0, 1])
+def test_full_beam_equals_exhaustive_with_fusion(mode, retract):
+    """With θ = ∞ and K = V'^T, every transcript's score = combine(acoustic) + α_LM·seq(y) +
+    α_BT·Σ deltas(y) + β|y| (SURVEY §8(c) pin 2), on the 3-gram fixture (a, b, c; blank = 3)."""
+    syms = ["a", "b", "c"]
+    path = os.path.join(GOLDEN, "arpa_3gram.arpa")
+    lm = oracle.LM(path, 3, syms)
+    py = ArpaPy(path)
+    phrases = [[0, 1], [1, 2], [0, 1, 2], [2, 2, 0]]
+    bt = oracle.Boost(phrases, 0.7, 3)
+    bpy = BoostPy(phrases, 0.7)
+    rng = np.random.default_rng(11 + mode + 2 * retract)
+    Vp1 = 4
+    for T in [1, 2, 3, 4, 5]:
+        D = _rand_logprobs(rng, T, Vp1)
+        cfg = oracle.make_cfg(Vp1 ** T, alpha_lm=0.6, alpha_bt=0.8, beta=0.3, merge_mode=mode, retract=retract)
+        res = dict(oracle.decode_nbest(D, cfg, lm=lm, boost=bt))
+        ex = exhaustive(D, Vp1 - 1, "lse" if mode == 0 else "max", alpha_lm=0.6, lm=py, symbols=syms,
+                        alpha_bt=0.8, boost=bpy, beta=0.3, retract=bool(retract))
+        assert set(res) == set(ex)
+        for y, s in ex.items():
+            assert res[y] == pytest.approx(s, abs=1e-10), (T, y)
+
+
+def test_lm_empty_utterance_score():
+    """L_b = 0 -> empty transcript with score α_LM·Final(<s>)."""
+    lm = oracle.LM(os.path.join(GOLDEN, "arpa_2gram.arpa"), 2, ["a", "b"])
+    D = np.zeros((3, 3))
+    res = oracle.decode_nbest(D, oracle.make_cfg(2, alpha_lm=0.5), lm=lm, L=0)
+    assert res == [((), pytest.approx(0.5 * -2.302585092994046, abs=1e-12))]
+
+
+# ---------------------------------------------------------------- synthetic LM is a normalised backoff LM
+
+@pytest.mark.slow
+def test_synthetic_arpa_normalised():
+    import synth
+    path = synth.arpa_file(V=1024)
+    lm = oracle.LM(path, 1024)
+    assert lm.order == 4
+    rng = np.random.default_rng(0)
+    src = synth.MarkovSource(1024, synth.LM_SEED)
+    hists = [[]] + [list(src.sequences(rng, 1, int(n))[0]) for n in [1, 2, 3, 5, 8]] + \
+            [list(rng.integers(0, 1024, 3))]
+    for h in hists:
+        tot = sum(math.exp(lm.logp(h, w)) for w in range(1024)) + math.exp(lm.logp(h, -1))
+        assert tot == pytest.approx(1.0, abs=1e-3), h

@@ -1,0 +1,364 @@
+// C ABI of libflexctc (include/flexctc.h): validation, handle management, device upload,
+// workspace layout, and the two launches of a decode. No compute happens on the host: the
+// builders only lay out the LM / boost tables, and flexctc_decode refuses host memory.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "flexctc_internal.h"
+
+namespace flexctc {
+
+thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+flexctc_status fail(flexctc_status st, const std::string& msg) {
+    g_error = msg;
+    return st;
+}
+
+namespace {
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+flexctc_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(e == cudaErrorMemoryAllocation ? FLEXCTC_ERR_OOM : FLEXCTC_ERR_CUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// one device allocation, arrays at 256-B aligned offsets
+struct Upload {
+    std::vector<std::pair<const void*, size_t>> parts;
+    size_t add(const void* p, size_t n) {
+        size_t off = 0;
+        for (auto& q : parts) off += align256(q.second);
+        parts.emplace_back(p, n);
+        return off;
+    }
+    size_t total() const {
+        size_t s = 0;
+        for (auto& q : parts) s += align256(q.second);
+        return s;
+    }
+};
+
+flexctc_status upload(int device, Upload& up, void** dmem) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    const size_t tot = std::max<size_t>(up.total(), 256);
+    e = cudaMalloc(dmem, tot);
+    if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "cudaMalloc"); }
+    size_t off = 0;
+    for (auto& q : up.parts) {
+        if (q.second) {
+            e = cudaMemcpy((char*)*dmem + off, q.first, q.second, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) { cudaFree(*dmem); *dmem = nullptr; cudaSetDevice(prev); return cuda_fail(e, "cudaMemcpy"); }
+        }
+        off += align256(q.second);
+    }
+    cudaSetDevice(prev);
+    return FLEXCTC_OK;
+}
+
+bool is_device_ptr(const void* p, int dev) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    if (a.type == cudaMemoryTypeManaged) return true;
+    return a.type == cudaMemoryTypeDevice && a.device == dev;
+}
+
+}  // namespace
+
+WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K) {
+    WorkspaceLayout w{};
+    w.nch = (T + kChunk - 1) / kChunk;
+    if (w.nch < 1) w.nch = 1;
+    size_t o = 0;
+    w.flags = o; o += align256(16);
+    w.order = o; o += align256(4 * (size_t)B);
+    w.len_c = o; o += align256(4 * (size_t)B);
+    w.chunk_anc = o; o += align256((size_t)B * w.nch * K);
+    w.bp_parent = o; o += align256((size_t)B * T * K);
+    w.bp_label = o; o += align256((size_t)B * T * K * 2);
+    w.align_ws = o; o += align256((size_t)B * T * 4);
+    w.total = o;
+    return w;
+}
+
+}  // namespace flexctc
+
+using namespace flexctc;
+
+extern "C" {
+
+const char* flexctc_last_error(void) { return g_error.c_str(); }
+const char* flexctc_version(void) { return "flexctc-b200 0.1 (sm_100a)"; }
+
+flexctc_status flexctc_lm_load(const char* arpa_path, int32_t vocab_size, const char* const* token_symbols,
+                               int32_t device, flexctc_lm** out) {
+    if (!out) return fail(FLEXCTC_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!arpa_path) return fail(FLEXCTC_ERR_INVALID_ARG, "arpa_path is NULL");
+    auto* lm = new flexctc_lm();
+    flexctc_status st = build_lm_host(arpa_path, vocab_size, token_symbols, lm->host);
+    if (st != FLEXCTC_OK) { delete lm; return st; }
+    lm->device = device;
+    if (device >= 0) {
+        const LmHost& h = lm->host;
+        Upload up;
+        size_t o_hdr = up.add(h.st_hdr.data(), h.st_hdr.size() * 4);
+        size_t o_tok = up.add(h.arc_tok.data(), h.arc_tok.size() * 2);
+        size_t o_val = up.add(h.arc_val.data(), h.arc_val.size() * 4);
+        size_t o_ulp = up.add(h.uni_lp.data(), h.uni_lp.size() * 4);
+        size_t o_unx = up.add(h.uni_next.data(), h.uni_next.size() * 4);
+        size_t o_eos = up.add(h.eos.data(), h.eos.size() * 4);
+        size_t o_ub = up.add(h.ub.data(), h.ub.size() * 4);
+        st = upload(device, up, &lm->dmem);
+        if (st != FLEXCTC_OK) { delete lm; return st; }
+        lm->dbytes = up.total();
+        char* d = (char*)lm->dmem;
+        lm->dev.st_hdr = (const int4*)(d + o_hdr);
+        lm->dev.arc_tok = (const uint16_t*)(d + o_tok);
+        lm->dev.arc_val = (const int2*)(d + o_val);
+        lm->dev.uni_lp = (const float*)(d + o_ulp);
+        lm->dev.uni_next = (const int32_t*)(d + o_unx);
+        lm->dev.eos = (const float*)(d + o_eos);
+        lm->dev.ub = (const float*)(d + o_ub);
+        lm->dev.start = h.start;
+    }
+    *out = lm;
+    return FLEXCTC_OK;
+}
+
+void flexctc_lm_free(flexctc_lm* lm) {
+    if (!lm) return;
+    if (lm->dmem) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(lm->device);
+        cudaFree(lm->dmem);
+        cudaSetDevice(prev);
+    }
+    delete lm;
+}
+
+flexctc_status flexctc_lm_get_info(const flexctc_lm* lm, flexctc_lm_info* info) {
+    if (!lm || !info) return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    info->order = lm->host.order;
+    info->vocab_size = lm->host.V;
+    info->n_states = lm->host.S;
+    info->start_state = lm->host.start;
+    info->n_arcs = (int64_t)lm->host.arc_tok.size();
+    info->device_bytes = (int64_t)lm->dbytes;
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_lm_host_query(const flexctc_lm* lm, int32_t state, int32_t token, float* logp,
+                                     int32_t* next_state) {
+    if (!lm || !logp || !next_state) return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    if (state < 0 || state >= lm->host.S) return fail(FLEXCTC_ERR_INVALID_ARG, "state out of range");
+    if (token == -1) {
+        *logp = lm->host.eos[state];
+        *next_state = state;
+        return FLEXCTC_OK;
+    }
+    if (token < 0 || token >= lm->host.V) return fail(FLEXCTC_ERR_INVALID_ARG, "token out of range");
+    *logp = lm_query_host(lm->host, state, token, next_state);
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_boost_build(const int32_t* tokens, const int64_t* offsets, int32_t n_phrases,
+                                   float token_weight, int32_t vocab_size, int32_t device, flexctc_boost** out) {
+    if (!out) return fail(FLEXCTC_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    auto* bt = new flexctc_boost();
+    flexctc_status st = build_boost_host(tokens, offsets, n_phrases, token_weight, vocab_size, bt->host);
+    if (st != FLEXCTC_OK) { delete bt; return st; }
+    bt->device = device;
+    if (device >= 0) {
+        const BoostHost& h = bt->host;
+        Upload up;
+        size_t o_tab = up.add(h.tab.data(), h.tab.size() * 4);
+        size_t o_u = up.add(h.U.data(), h.U.size() * 4);
+        size_t o_m = up.add(h.maxd.data(), h.maxd.size() * 4);
+        st = upload(device, up, &bt->dmem);
+        if (st != FLEXCTC_OK) { delete bt; return st; }
+        bt->dbytes = up.total();
+        char* d = (char*)bt->dmem;
+        bt->dev.tab = (const int2*)(d + o_tab);
+        bt->dev.U = (const float*)(d + o_u);
+        bt->dev.maxd = (const float*)(d + o_m);
+        bt->dev.V = h.V;
+    }
+    *out = bt;
+    return FLEXCTC_OK;
+}
+
+void flexctc_boost_free(flexctc_boost* bt) {
+    if (!bt) return;
+    if (bt->dmem) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(bt->device);
+        cudaFree(bt->dmem);
+        cudaSetDevice(prev);
+    }
+    delete bt;
+}
+
+flexctc_status flexctc_boost_host_query(const flexctc_boost* bt, int32_t node, int32_t token, float* delta,
+                                        int32_t* next_node, float* U_node) {
+    if (!bt || !delta || !next_node || !U_node) return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    const BoostHost& h = bt->host;
+    if (node < 0 || node >= h.N || token < 0 || token >= h.V) return fail(FLEXCTC_ERR_INVALID_ARG, "node/token out of range");
+    const size_t e = ((size_t)node * h.V + token) * 2;
+    *next_node = h.tab[e];
+    memcpy(delta, &h.tab[e + 1], 4);
+    *U_node = h.U[node];
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_boost_num_nodes(const flexctc_boost* bt, int32_t* n_nodes) {
+    if (!bt || !n_nodes) return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    *n_nodes = bt->host.N;
+    return FLEXCTC_OK;
+}
+
+size_t flexctc_workspace_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg) {
+    (void)Vp1;
+    if (!cfg || B < 0 || T < 0 || cfg->beam < 1) return 0;
+    return workspace_layout(B, T, cfg->beam).total;
+}
+
+static flexctc_status validate_cfg(const flexctc_config* cfg) {
+    if (!cfg) return fail(FLEXCTC_ERR_INVALID_ARG, "cfg is NULL");
+    if (cfg->beam < 1) return fail(FLEXCTC_ERR_INVALID_ARG, "beam must be >= 1");
+    if (cfg->beam > kMaxBeam) return fail(FLEXCTC_ERR_CAPACITY, "beam > 256");
+    if (!(cfg->theta >= 0.0f)) return fail(FLEXCTC_ERR_INVALID_ARG, "theta must be >= 0 (or +inf)");
+    if (cfg->merge_mode != 0 && cfg->merge_mode != 1) return fail(FLEXCTC_ERR_INVALID_ARG, "merge_mode must be 0 or 1");
+    if (!std::isfinite(cfg->alpha_lm) || !std::isfinite(cfg->alpha_bt) || !std::isfinite(cfg->beta))
+        return fail(FLEXCTC_ERR_INVALID_ARG, "alpha/beta must be finite");
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lengths,
+                              int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
+                              const flexctc_boost* boost, void* workspace, size_t workspace_bytes,
+                              flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                              float* out_scores, int32_t* out_timestamps, int32_t* out_alignment) {
+    flexctc_status st = validate_cfg(cfg);
+    if (st != FLEXCTC_OK) return st;
+    if (B < 0 || T < 0) return fail(FLEXCTC_ERR_INVALID_ARG, "B and T must be >= 0");
+    if (Vp1 < 2) return fail(FLEXCTC_ERR_INVALID_ARG, "Vp1 must be >= 2");
+    if (Vp1 > kMaxVp1) return fail(FLEXCTC_ERR_CAPACITY, "Vp1 > 8192");
+    if (stride_t < Vp1 || stride_b < (int64_t)T * stride_t) return fail(FLEXCTC_ERR_INVALID_ARG, "strides overlap rows");
+    if ((int64_t)Vp1 * cfg->beam >= (int64_t)0xffffffff) return fail(FLEXCTC_ERR_CAPACITY, "K*Vp1 too large");
+    const WorkspaceLayout wl = workspace_layout(B, T, cfg->beam);
+    if (!workspace || workspace_bytes < wl.total)
+        return fail(FLEXCTC_ERR_CAPACITY, "workspace smaller than flexctc_workspace_bytes()");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (B == 0) return FLEXCTC_OK;
+    if (!is_device_ptr(log_probs, dev) || !is_device_ptr(lengths, dev) || !is_device_ptr(workspace, dev) ||
+        !is_device_ptr(out_tokens, dev) || !is_device_ptr(out_num_tokens, dev) || !is_device_ptr(out_scores, dev) ||
+        (out_timestamps && !is_device_ptr(out_timestamps, dev)) || (out_alignment && !is_device_ptr(out_alignment, dev)))
+        return fail(FLEXCTC_ERR_INVALID_ARG, "every buffer must be device memory of the current device (no CPU path)");
+    if (lm) {
+        if (lm->device != dev || !lm->dmem) return fail(FLEXCTC_ERR_INVALID_ARG, "LM handle belongs to another device");
+        if (lm->host.V != Vp1 - 1) return fail(FLEXCTC_ERR_INVALID_ARG, "LM vocab_size != Vp1-1");
+    }
+    if (boost) {
+        if (boost->device != dev || !boost->dmem) return fail(FLEXCTC_ERR_INVALID_ARG, "boost handle belongs to another device");
+        if (boost->host.V != Vp1 - 1) return fail(FLEXCTC_ERR_INVALID_ARG, "boost vocab_size != Vp1-1");
+    }
+    DecodeParams p{};
+    p.log_probs = log_probs;
+    p.stride_b = stride_b;
+    p.stride_t = stride_t;
+    p.lengths = lengths;
+    p.B = B; p.T = T; p.Vp1 = Vp1; p.K = cfg->beam;
+    p.alpha_lm = cfg->alpha_lm; p.alpha_bt = cfg->alpha_bt; p.beta = cfg->beta; p.theta = cfg->theta;
+    p.merge_mode = cfg->merge_mode; p.retract = cfg->retract_boost_at_eos;
+    p.use_lm = lm != nullptr; p.use_bt = boost != nullptr;
+    if (lm) p.lm = lm->dev;
+    if (boost) p.bt = boost->dev;
+    char* w = (char*)workspace;
+    p.flags = (uint32_t*)(w + wl.flags);
+    p.order = (int32_t*)(w + wl.order);
+    p.len_c = (int32_t*)(w + wl.len_c);
+    p.chunk_anc = (uint8_t*)(w + wl.chunk_anc);
+    p.bp_parent = (uint8_t*)(w + wl.bp_parent);
+    p.bp_label = (uint16_t*)(w + wl.bp_label);
+    p.align_ws = (int32_t*)(w + wl.align_ws);
+    p.nch = wl.nch;
+    p.out_tokens = out_tokens; p.out_num = out_num_tokens; p.out_scores = out_scores;
+    p.out_ts = out_timestamps; p.out_align = out_alignment;
+    std::string err;
+    int rc = launch_decode(p, (void*)stream, err);
+    if (rc == 2) return fail(FLEXCTC_ERR_CAPACITY, err);
+    if (rc != 0) return fail(FLEXCTC_ERR_CUDA, err);
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags) {
+    if (!workspace || !device_flags) return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    cudaError_t e = cudaMemcpy(device_flags, workspace, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy");
+    return FLEXCTC_OK;
+}
+
+size_t flexctc_host_scratch_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg) {
+    if (!cfg || B < 0 || T < 0 || Vp1 < 2 || cfg->beam < 1) return 0;
+    size_t s = align256((size_t)B * T * Vp1 * 4) + align256((size_t)B * 4);
+    s += align256((size_t)B * T * 4) * 2 + align256((size_t)B * 4) * 2;
+    s += workspace_layout(B, T, cfg->beam).total;
+    return s;
+}
+
+flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* lengths_host, int32_t B, int32_t T,
+                                   int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
+                                   const flexctc_boost* boost, void* device_scratch, size_t scratch_bytes,
+                                   flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                                   float* out_scores, int32_t* out_timestamps) {
+    flexctc_status st = validate_cfg(cfg);
+    if (st != FLEXCTC_OK) return st;
+    if (B < 0 || T < 0 || Vp1 < 2) return fail(FLEXCTC_ERR_INVALID_ARG, "bad shape");
+    const size_t need = flexctc_host_scratch_bytes(B, T, Vp1, cfg);
+    if (!device_scratch || scratch_bytes < need) return fail(FLEXCTC_ERR_CAPACITY, "device_scratch too small");
+    if (!log_probs_host || !lengths_host || !out_tokens || !out_num_tokens || !out_scores)
+        return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    if (B == 0) return FLEXCTC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    char* d = (char*)device_scratch;
+    size_t o = 0;
+    float* dD = (float*)(d + o); o += align256((size_t)B * T * Vp1 * 4);
+    int32_t* dL = (int32_t*)(d + o); o += align256((size_t)B * 4);
+    int32_t* dTok = (int32_t*)(d + o); o += align256((size_t)B * T * 4);
+    int32_t* dTs = (int32_t*)(d + o); o += align256((size_t)B * T * 4);
+    int32_t* dN = (int32_t*)(d + o); o += align256((size_t)B * 4);
+    float* dS = (float*)(d + o); o += align256((size_t)B * 4);
+    void* ws = d + o;
+    const size_t wsb = scratch_bytes - o;
+    cudaError_t e = cudaMemcpyAsync(dD, log_probs_host, (size_t)B * T * Vp1 * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dL, lengths_host, (size_t)B * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+    st = flexctc_decode(dD, (int64_t)T * Vp1, Vp1, dL, B, T, Vp1, cfg, lm, boost, ws, wsb, stream, dTok, dN, dS,
+                        out_timestamps ? dTs : nullptr, nullptr);
+    if (st != FLEXCTC_OK) return st;
+    e = cudaMemcpyAsync(out_tokens, dTok, (size_t)B * T * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_num_tokens, dN, (size_t)B * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_scores, dS, (size_t)B * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && out_timestamps)
+        e = cudaMemcpyAsync(out_timestamps, dTs, (size_t)B * T * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "decode_host copy/sync");
+    return FLEXCTC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// Internal definitions of libflexctc (product code; never shared with oracle/).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <vector_types.h>
+
+#include "../../include/flexctc.h"
+
+namespace flexctc {
+
+void set_error(const std::string& msg);
+flexctc_status fail(flexctc_status st, const std::string& msg);
+
+// ---------------------------------------------------------------------------------------
+// LM device layout ("sorted-arc, state-indexed"; DESIGN.md §Data layout)
+//   state header  int4 {arc_off, arc_deg, backoff_state, backoff_weight(f32 bits)}
+//   arcs          arc_tok u16 (decoder token, sorted within a state) + arc_val {f32 logp, i32 next}
+//   root row      dense uni_lp[V], uni_next[V] (the unigram level)
+//   per state     eos[S] = LM.Final and lm_ub[S] >= max_w log P(w | s) (pre-prune bound)
+// State 0 is the root (empty context); it has no CSR arcs (the dense row replaces them).
+// ---------------------------------------------------------------------------------------
+struct LmHost {
+    int32_t order = 0, V = 0, S = 0, start = 0;
+    std::vector<int32_t> st_hdr;   // 4 ints per state
+    std::vector<uint16_t> arc_tok;
+    std::vector<int32_t> arc_val;  // 2 ints per arc: f32 bits, next
+    std::vector<float> uni_lp;
+    std::vector<int32_t> uni_next;
+    std::vector<float> eos, ub;
+};
+
+struct LmDev {
+    const int4* st_hdr;
+    const uint16_t* arc_tok;
+    const int2* arc_val;
+    const float* uni_lp;
+    const int32_t* uni_next;
+    const float* eos;
+    const float* ub;
+    int32_t start;
+};
+
+// ---------------------------------------------------------------------------------------
+// Boost device layout: full Aho-Corasick transition table [nodes x V] of {next, f32 delta}
+// (delta = dC(v) + U(v) - U(u), reading R17), plus U[n] and maxd[n] = max_w delta(n, w).
+// ---------------------------------------------------------------------------------------
+struct BoostHost {
+    int32_t V = 0, N = 0;
+    std::vector<int32_t> tab;  // 2 ints per (node, token)
+    std::vector<float> U, maxd;
+};
+
+struct BoostDev {
+    const int2* tab;
+    const float* U;
+    const float* maxd;
+    int32_t V;
+};
+
+flexctc_status build_lm_host(const char* path, int32_t V, const char* const* syms, LmHost& out);
+flexctc_status build_boost_host(const int32_t* toks, const int64_t* offs, int32_t n, float w, int32_t V,
+                                BoostHost& out);
+
+// host mirrors of the device queries (same arithmetic order), used by the inspection API
+float lm_query_host(const LmHost& lm, int32_t s, int32_t w, int32_t* next);
+
+// ---------------------------------------------------------------------------------------
+// Decode kernel parameters
+// ---------------------------------------------------------------------------------------
+constexpr int kChunk = 32;      // frames per backtrace chunk (chunk ancestors, §7.3 item 6)
+constexpr int kMaxBeam = 256;   // parent index fits a u8
+constexpr int kMaxVp1 = 8192;   // frame rows are staged in shared memory
+
+struct DecodeParams {
+    const float* log_probs;
+    int64_t stride_b, stride_t;
+    const int32_t* lengths;
+    int32_t B, T, Vp1, K;
+    float alpha_lm, alpha_bt, beta, theta;
+    int32_t merge_mode, retract;
+    int32_t use_lm, use_bt;
+    LmDev lm;
+    BoostDev bt;
+    // workspace
+    uint32_t* flags;      // [0] flags, [1] work queue
+    int32_t* order;       // [B] utterances by length, longest first
+    int32_t* len_c;       // [B] clamped lengths
+    uint8_t* chunk_anc;   // [B][nch][K]
+    uint8_t* bp_parent;   // [B][T][K]
+    uint16_t* bp_label;   // [B][T][K]
+    int32_t* align_ws;    // [B][T]
+    int32_t nch;
+    // outputs
+    int32_t* out_tokens;
+    int32_t* out_num;
+    float* out_scores;
+    int32_t* out_ts;
+    int32_t* out_align;   // may alias align_ws
+};
+
+struct WorkspaceLayout {
+    size_t flags, order, len_c, chunk_anc, bp_parent, bp_label, align_ws, total;
+    int32_t nch;
+};
+WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K);
+
+// launches (beam_kernel.cu)
+int launch_decode(const DecodeParams& p, void* stream, std::string& err);
+
+}  // namespace flexctc
+
+struct flexctc_lm {
+    int32_t device = -1;
+    flexctc::LmHost host;
+    void* dmem = nullptr;  // one device allocation holding every array
+    size_t dbytes = 0;
+    flexctc::LmDev dev{};
+};
+
+struct flexctc_boost {
+    int32_t device = -1;
+    flexctc::BoostHost host;
+    void* dmem = nullptr;
+    size_t dbytes = 0;
+    flexctc::BoostDev dev{};
+};

@@ -1,0 +1,265 @@
+"""Thin Python binding of libflexctc.so (include/flexctc.h): argument marshalling only.
+
+Every step of the decode runs in the library's CUDA kernels; torch provides device memory and
+streams. There is no CPU path: if the shared library is missing or cannot be loaded, importing
+this module raises, and `decode` refuses tensors that are not on a CUDA device.
+
+Names follow the C ABI: lm_load, boost_build, decode, decode_host, workspace_bytes, check.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+FLEXCTC_OK = 0
+_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "PARSE", 3: "VOCAB_BIND", 4: "CAPACITY", 5: "CUDA", 6: "OOM", 7: "IO"}
+FLAG_LENGTH_CLAMPED_HIGH = 1
+FLAG_LENGTH_CLAMPED_LOW = 2
+
+
+class FlexCTCError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"flexctc {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    """flexctc_config (Eq. (1) weights P:96-98, θ P:237)."""
+    _fields_ = [("beam", ctypes.c_int32), ("alpha_lm", ctypes.c_float), ("alpha_bt", ctypes.c_float),
+                ("beta", ctypes.c_float), ("theta", ctypes.c_float), ("merge_mode", ctypes.c_int32),
+                ("retract_boost_at_eos", ctypes.c_int32)]
+
+
+def config(beam: int, alpha_lm: float = 0.0, alpha_bt: float = 0.0, beta: float = 0.0,
+           theta: float = 12.0, merge_mode: int = 0, retract_boost_at_eos: int = 0) -> Config:
+    return Config(int(beam), float(alpha_lm), float(alpha_bt), float(beta), float(theta), int(merge_mode),
+                  int(retract_boost_at_eos))
+
+
+class LmInfo(ctypes.Structure):
+    _fields_ = [("order", ctypes.c_int32), ("vocab_size", ctypes.c_int32), ("n_states", ctypes.c_int32),
+                ("start_state", ctypes.c_int32), ("n_arcs", ctypes.c_int64), ("device_bytes", ctypes.c_int64)]
+
+
+EXPORTS = [
+    "flexctc_last_error", "flexctc_version", "flexctc_lm_load", "flexctc_lm_free", "flexctc_lm_get_info",
+    "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
+    "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
+    "flexctc_host_scratch_bytes", "flexctc_decode_host",
+]
+
+
+def _load() -> ctypes.CDLL:
+    path = _build.LIB
+    if not os.path.exists(path):
+        _build.build()  # nvcc is part of the image; a failure here raises loudly
+    L = ctypes.CDLL(path)
+    vp, i32, i64, f32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
+    P = ctypes.POINTER
+    L.flexctc_last_error.restype = ctypes.c_char_p
+    L.flexctc_version.restype = ctypes.c_char_p
+    L.flexctc_lm_load.argtypes = [ctypes.c_char_p, i32, vp, i32, P(vp)]
+    L.flexctc_lm_free.argtypes = [vp]
+    L.flexctc_lm_free.restype = None
+    L.flexctc_lm_get_info.argtypes = [vp, P(LmInfo)]
+    L.flexctc_lm_host_query.argtypes = [vp, i32, i32, P(f32), P(i32)]
+    L.flexctc_boost_build.argtypes = [vp, vp, i32, f32, i32, i32, P(vp)]
+    L.flexctc_boost_free.argtypes = [vp]
+    L.flexctc_boost_free.restype = None
+    L.flexctc_boost_host_query.argtypes = [vp, i32, i32, P(f32), P(i32), P(f32)]
+    L.flexctc_boost_num_nodes.argtypes = [vp, P(i32)]
+    L.flexctc_workspace_bytes.argtypes = [i32, i32, i32, P(Config)]
+    L.flexctc_workspace_bytes.restype = sz
+    L.flexctc_decode.argtypes = [vp, i64, i64, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp,
+                                 vp, vp, vp, vp, vp]
+    L.flexctc_check.argtypes = [vp, P(ctypes.c_uint32)]
+    L.flexctc_host_scratch_bytes.argtypes = [i32, i32, i32, P(Config)]
+    L.flexctc_host_scratch_bytes.restype = sz
+    L.flexctc_decode_host.argtypes = [vp, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, vp, vp, vp, vp]
+    for name in EXPORTS:
+        getattr(L, name)  # AttributeError if a declared symbol is missing
+    return L
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    return lib.flexctc_last_error().decode()
+
+
+def _check(st: int):
+    if st != FLEXCTC_OK:
+        raise FlexCTCError(st, last_error())
+
+
+def version() -> str:
+    return lib.flexctc_version().decode()
+
+
+class LM:
+    """flexctc_lm handle (flexctc_lm_load). device=-1 builds a host-only handle for inspection."""
+
+    def __init__(self, arpa_path: str, vocab_size: int, symbols=None, device: int = 0):
+        syms = None
+        if symbols is not None:
+            self._syms = (ctypes.c_char_p * vocab_size)(*[s.encode() for s in symbols])
+            syms = ctypes.cast(self._syms, ctypes.c_void_p)
+        h = ctypes.c_void_p()
+        _check(lib.flexctc_lm_load(arpa_path.encode(), int(vocab_size), syms, int(device), ctypes.byref(h)))
+        self.h = h
+        self.vocab_size = vocab_size
+        self.device = device
+
+    def __del__(self):
+        if getattr(self, "h", None) and lib is not None:
+            lib.flexctc_lm_free(self.h)
+            self.h = None
+
+    def info(self) -> LmInfo:
+        i = LmInfo()
+        _check(lib.flexctc_lm_get_info(self.h, ctypes.byref(i)))
+        return i
+
+    def host_query(self, state: int, token: int):
+        lp, nx = ctypes.c_float(), ctypes.c_int32()
+        _check(lib.flexctc_lm_host_query(self.h, int(state), int(token), ctypes.byref(lp), ctypes.byref(nx)))
+        return lp.value, nx.value
+
+
+class Boost:
+    """flexctc_boost handle (flexctc_boost_build)."""
+
+    def __init__(self, phrases, token_weight: float, vocab_size: int, device: int = 0):
+        toks = np.ascontiguousarray([t for p in phrases for t in p], dtype=np.int32)
+        offs = np.zeros(len(phrases) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([len(p) for p in phrases])
+        h = ctypes.c_void_p()
+        _check(lib.flexctc_boost_build(toks.ctypes.data_as(ctypes.c_void_p), offs.ctypes.data_as(ctypes.c_void_p),
+                                       len(phrases), float(token_weight), int(vocab_size), int(device),
+                                       ctypes.byref(h)))
+        self.h = h
+        self.vocab_size = vocab_size
+
+    def __del__(self):
+        if getattr(self, "h", None) and lib is not None:
+            lib.flexctc_boost_free(self.h)
+            self.h = None
+
+    def num_nodes(self) -> int:
+        n = ctypes.c_int32()
+        _check(lib.flexctc_boost_num_nodes(self.h, ctypes.byref(n)))
+        return n.value
+
+    def host_query(self, node: int, token: int):
+        d, nx, u = ctypes.c_float(), ctypes.c_int32(), ctypes.c_float()
+        _check(lib.flexctc_boost_host_query(self.h, int(node), int(token), ctypes.byref(d), ctypes.byref(nx),
+                                            ctypes.byref(u)))
+        return d.value, nx.value, u.value
+
+
+def workspace_bytes(B: int, T: int, Vp1: int, cfg: Config) -> int:
+    return int(lib.flexctc_workspace_bytes(int(B), int(T), int(Vp1), ctypes.byref(cfg)))
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@dataclass
+class Workspace:
+    buf: object  # torch.uint8 cuda tensor
+    nbytes: int
+
+
+def make_workspace(B: int, T: int, Vp1: int, cfg: Config, device=None):
+    import torch
+    n = workspace_bytes(B, T, Vp1, cfg)
+    return Workspace(torch.empty(max(n, 1), dtype=torch.uint8, device=device or "cuda"), n)
+
+
+def decode(log_probs, lengths, cfg: Config, lm: LM | None = None, boost: Boost | None = None,
+           Vp1: int | None = None, workspace: Workspace | None = None, stream=None, outputs=None,
+           alignment: bool = False):
+    """Enqueue flexctc_decode on `stream` (default: torch's current stream).
+
+    log_probs: CUDA float32 tensor [B, T, >=Vp1] with unit stride on the last axis (the first
+    Vp1 columns are used; blank = Vp1-1). lengths: CUDA int32 [B]. Returns a dict of CUDA
+    tensors (tokens, num_tokens, scores, timestamps[, alignment]); valid once the stream syncs.
+    """
+    import torch
+    if not (log_probs.is_cuda and lengths.is_cuda):
+        raise FlexCTCError(1, "decode needs CUDA tensors (there is no CPU path)")
+    if log_probs.dtype != torch.float32 or log_probs.dim() != 3 or log_probs.stride(2) != 1:
+        raise FlexCTCError(1, "log_probs must be float32 [B, T, V'] with unit stride on V'")
+    if lengths.dtype != torch.int32:
+        raise FlexCTCError(1, "lengths must be int32")
+    B, T, W = log_probs.shape
+    Vp1 = W if Vp1 is None else Vp1
+    dev = log_probs.device
+    if workspace is None:
+        workspace = make_workspace(B, T, Vp1, cfg, dev)
+    if outputs is None:
+        outputs = {
+            "tokens": torch.empty((B, T), dtype=torch.int32, device=dev),
+            "num_tokens": torch.empty(B, dtype=torch.int32, device=dev),
+            "scores": torch.empty(B, dtype=torch.float32, device=dev),
+            "timestamps": torch.empty((B, T), dtype=torch.int32, device=dev),
+        }
+        if alignment:
+            outputs["alignment"] = torch.empty((B, T), dtype=torch.int32, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        _check(lib.flexctc_decode(_ptr(log_probs), log_probs.stride(0), log_probs.stride(1), _ptr(lengths), B, T,
+                                  Vp1, ctypes.byref(cfg), lm.h if lm else None, boost.h if boost else None,
+                                  _ptr(workspace.buf), workspace.nbytes, ctypes.c_void_p(stream.cuda_stream),
+                                  _ptr(outputs["tokens"]), _ptr(outputs["num_tokens"]), _ptr(outputs["scores"]),
+                                  _ptr(outputs.get("timestamps")), _ptr(outputs.get("alignment"))))
+    return outputs
+
+
+def check(workspace: Workspace) -> int:
+    """Device flags of the last decode on `workspace` (call after the stream has synchronised)."""
+    f = ctypes.c_uint32()
+    _check(lib.flexctc_check(_ptr(workspace.buf), ctypes.byref(f)))
+    return f.value
+
+
+def host_scratch_bytes(B: int, T: int, Vp1: int, cfg: Config) -> int:
+    return int(lib.flexctc_host_scratch_bytes(int(B), int(T), int(Vp1), ctypes.byref(cfg)))
+
+
+def decode_host(log_probs: np.ndarray, lengths: np.ndarray, cfg: Config, lm: LM | None = None,
+                boost: Boost | None = None, scratch=None, stream=None, out=None):
+    """End-to-end flexctc_decode_host: host (ideally pinned) float32 [B, T, V'] in, host outputs
+    out; H2D, decode and D2H all run inside the call (which synchronises the stream)."""
+    import torch
+    if isinstance(log_probs, np.ndarray):
+        log_probs = torch.from_numpy(log_probs)
+    if isinstance(lengths, np.ndarray):
+        lengths = torch.from_numpy(lengths)
+    assert log_probs.dtype == torch.float32 and log_probs.is_contiguous() and not log_probs.is_cuda
+    assert lengths.dtype == torch.int32 and lengths.is_contiguous() and not lengths.is_cuda
+    B, T, Vp1 = log_probs.shape
+    if scratch is None:
+        scratch = torch.empty(max(host_scratch_bytes(B, T, Vp1, cfg), 1), dtype=torch.uint8, device="cuda")
+    if out is None:
+        pin = log_probs.is_pinned()
+        out = {"tokens": torch.empty((B, T), dtype=torch.int32, pin_memory=pin),
+               "num_tokens": torch.empty(B, dtype=torch.int32, pin_memory=pin),
+               "scores": torch.empty(B, dtype=torch.float32, pin_memory=pin),
+               "timestamps": torch.empty((B, T), dtype=torch.int32, pin_memory=pin)}
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    _check(lib.flexctc_decode_host(_ptr(log_probs), _ptr(lengths), B, T, Vp1, ctypes.byref(cfg),
+                                   lm.h if lm else None, boost.h if boost else None, _ptr(scratch),
+                                   scratch.numel(), ctypes.c_void_p(stream.cuda_stream), _ptr(out["tokens"]),
+                                   _ptr(out["num_tokens"]), _ptr(out["scores"]), _ptr(out["timestamps"])))
+    return out

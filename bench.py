@@ -1,0 +1,342 @@
+"""Benchmark of the FlexCTC hot path on B200 (driver contract).
+
+One step = one flexctc_decode of the whole hot path (Alg. 1 over every frame of every
+utterance of the rank's batch: frame read, candidates, LM/boost fusion, top-K, θ-prune, state
+advance, recombination, EOS, backtrace) with inputs already resident in HBM. L2 is flushed
+between steps (a 256 MiB write). Default workload: c4 = BASELINE.json configs[3] (B=64 per GPU,
+T=400 @ 40 ms, V=1024+blank, beam 16, 4-gram LM, 1000 boosted phrases) — the configuration the
+north-star metric is quoted on. Multi-GPU (torchrun): weak scaling, each rank decodes its own
+c4 batch (distinct seeds), LM/boost replicated, results gathered once at the end.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4] [--impl flexctc|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "RTFx (audio s decoded / wall s) and frames·beams/s at 1/2/4/8 B200"
+UNIT = "RTFx"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c4", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--impl", default="flexctc", choices=["flexctc", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0 = auto)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(wl, B, T, Lsum, extra=None):
+    cfg = {"workload": wl.name, "B_per_gpu": B, "T": T, "V": wl.V, "beam": wl.beam,
+           "lm": "synthetic 4-gram ARPA (~1.08M n-grams)" if wl.lm else None,
+           "phrases": 1000 if wl.boost else 0, "alpha_lm": wl.alpha_lm if wl.lm else 0.0,
+           "alpha_bt": wl.alpha_bt if wl.boost else 0.0, "beta": wl.beta, "theta": wl.theta,
+           "merge": "lse" if wl.merge_mode == 0 else "max", "frame_s": synth.FRAME_SECONDS,
+           "frames_per_gpu": int(Lsum), "l2": "flushed (256 MiB write) between timed steps"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 7:
+                for n, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(workload)
+    if not e:
+        return None, None
+    return e.get("dram_bytes_per_launch"), e.get("source")
+
+
+def cpu_baseline(wl, D, L, arpa, ph, n_utts):
+    """The oracle as it stands (never tuned), on this host's cores, over a bounded sample."""
+    import oracle
+    lm = oracle.LM(arpa, wl.V) if wl.lm else None
+    bt = oracle.Boost(ph, 1.0, wl.V) if wl.boost else None
+    cfg = oracle.make_cfg(wl.beam, wl.alpha_lm if wl.lm else 0.0, wl.alpha_bt if wl.boost else 0.0, wl.beta,
+                          wl.theta, wl.merge_mode)
+    cores = os.cpu_count() or 1
+    idx = np.arange(min(n_utts, D.shape[0]))
+    Ds = np.ascontiguousarray(D[idx])
+    t0 = time.perf_counter()
+    oracle.decode(Ds, L[idx], cfg, lm, bt, nthreads=cores)
+    dt = time.perf_counter() - t0
+    audio = float(L[idx].sum()) * synth.FRAME_SECONDS
+    return {"value": audio / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{len(idx)} of the {wl.name} utterances ({int(L[idx].sum())} frames, "
+                      f"{audio:.1f} audio s) decoded by the C++ oracle on {cores} host threads in {dt:.1f} s",
+            "frames_beams_per_s": float(L[idx].sum()) * wl.beam / dt}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    wl = synth.WORKLOADS[args.workload]
+    _, D, L, arpa, ph = synth.workload_inputs(args.workload)
+    import oracle
+    lm = oracle.LM(arpa, wl.V) if wl.lm else None
+    bt = oracle.Boost(ph, 1.0, wl.V) if wl.boost else None
+    cfg = oracle.make_cfg(wl.beam, wl.alpha_lm if wl.lm else 0.0, wl.alpha_bt if wl.boost else 0.0, wl.beta,
+                          wl.theta, wl.merge_mode)
+    cores = os.cpu_count() or 1
+    n = args.cpu_sample or max(1, min(wl.B, cores))
+    idx = np.arange(n)
+    Ds = np.ascontiguousarray(D[idx])
+    for _ in range(args.warmup):
+        oracle.decode(Ds, L[idx], cfg, lm, bt, nthreads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.decode(Ds, L[idx], cfg, lm, bt, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    frames = float(L[idx].sum())
+    value = frames * synth.FRAME_SECONDS * args.steps / tot
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": workload_config(wl, int(n), int(D.shape[1]), L[idx].sum(),
+                                     {"reference": "C++ oracle (oracle/oracle.cpp), host cores"}),
+           "frames_beams_per_s": frames * wl.beam * args.steps / tot,
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"{n} utterances of {wl.name} per step on {cores} host threads"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_flexctc(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_07315_b200 as F
+    from paper_2508_07315_b200 import flexctc as FX
+    from paper_2508_07315_b200.shard import gather_results
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "--gpus must match WORLD_SIZE under torchrun"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = synth.WORKLOADS[args.workload]
+    # weak scaling: rank r decodes its own batch of the workload (seed offset r)
+    _, D, L, arpa, ph = synth.workload_inputs(args.workload, seed_offset=rank)
+    B, T, Vp1 = D.shape
+    lm = F.LM(arpa, wl.V, device=local) if wl.lm else None
+    bt = F.Boost(ph, 1.0, wl.V, device=local) if wl.boost else None
+    cfg = F.config(wl.beam, wl.alpha_lm if wl.lm else 0.0, wl.alpha_bt if wl.boost else 0.0, wl.beta, wl.theta,
+                   wl.merge_mode)
+    Dd = torch.from_numpy(D).to(dev)
+    Ld = torch.from_numpy(L).to(dev)
+    ws = F.make_workspace(B, T, Vp1, cfg, dev)
+    stream = torch.cuda.Stream(dev)
+    out = None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def step(e=None):
+        nonlocal out
+        with torch.cuda.stream(stream):
+            flush.fill_(1)  # evict L2 (126 MB) between steps; not timed
+            if e is not None:
+                e[0].record(stream)
+                FX.set_profile_events(e[2], e[3])
+            out = F.decode(Dd, Ld, cfg, lm, bt, workspace=ws, stream=stream, outputs=out)
+            if e is not None:
+                e[1].record(stream)
+                FX.set_profile_events(None, None)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    for i in range(args.steps):
+        step(ev[i])
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_dec = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3        # s, whole decode per step summed
+    t_kern = sum(e[2].elapsed_time(e[3]) for e in ev) / 1e3       # s, beam kernel only
+    flags = F.check(ws)
+    tt = torch.tensor([t_dec, t_kern], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_dec, t_kern = float(tt[0]), float(tt[1])
+    frames_local = float(L.sum())
+    frames_all = frames_local * world  # weak scaling: same frame count per rank (c4: fixed T)
+    if world > 1:
+        fa = torch.tensor([frames_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(fa)
+        frames_all = float(fa[0])
+    value = frames_all * synth.FRAME_SECONDS * args.steps / t_dec
+    fbps = frames_all * wl.beam * args.steps / t_dec
+
+    # roofline of the dominant kernel (the persistent beam kernel): algorithmic bytes per launch =
+    # Σ_b L_b · (4·V' [read D once] + 3·K [u8 parent + u16 label backpointers])
+    alg_bytes = frames_local * (4 * Vp1 + 3 * wl.beam)
+    kern_s = t_kern / args.steps
+    achieved = alg_bytes / kern_s / 1e9
+    peak, peak_src = peaks()
+    traffic, traffic_src = ncu_traffic(args.workload)
+
+    # e2e through the public host-buffer entry (flexctc_decode_host): H2D + decode + D2H per step
+    e2e = None
+    if not args.no_e2e:
+        Dp = torch.from_numpy(D).pin_memory()
+        Lp = torch.from_numpy(L).pin_memory()
+        scratch = torch.empty(F.host_scratch_bytes(B, T, Vp1, cfg), dtype=torch.uint8, device=dev)
+        hout = None
+        for _ in range(max(1, args.warmup)):
+            hout = F.decode_host(Dp, Lp, cfg, lm, bt, scratch=scratch, stream=stream, out=hout)
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            stream.synchronize()
+            t0 = time.perf_counter()
+            hout = F.decode_host(Dp, Lp, cfg, lm, bt, scratch=scratch, stream=stream, out=hout)
+            ts.append(time.perf_counter() - t0)
+        te = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": frames_all * synth.FRAME_SECONDS * args.steps / float(te[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int(D.nbytes + L.nbytes),
+               "d2h_bytes_per_step": int(B * T * 4 * 2 + B * 4 * 2),
+               "path": "flexctc_decode_host (pinned host buffers, copies + decode + sync inside)"}
+
+    # gather the final results (the only cross-GPU traffic)
+    gathered = None
+    if world > 1:
+        g = gather_results({k: v for k, v in out.items()}, np.arange(rank * B, rank * B + B), B * world, T, device=dev)
+        gathered = int(g["num_tokens"].sum().item())
+
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_dec / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(wl, B, T, frames_local, {"parallelism": f"dp{world} (utterance shards)"}),
+            "frames_beams_per_s": fbps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "ctc_beam_kernel (persistent)", "kernel_ms": 1e3 * kern_s,
+                         "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                         "traffic_source": traffic_src,
+                         "note": "latency-bound recurrence: T_max dependent frame steps; see DESIGN.md"},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk,
+            "e2e": e2e,
+            "device_flags": flags,
+        }
+        if gathered is not None:
+            res["gathered_tokens"] = gathered
+        if world == 1 and not args.no_cpu_baseline:
+            n = args.cpu_sample or max(1, min(B, os.cpu_count() or 1))
+            res["cpu_baseline"] = cpu_baseline(wl, D, L, arpa, ph, n)
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_flexctc(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -148,6 +148,12 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
                               int32_t* out_tokens, int32_t* out_num_tokens, float* out_scores,
                               int32_t* out_timestamps, int32_t* out_alignment);
 
+/* Measurement hook: when both are non-NULL, subsequent flexctc_decode calls on this thread
+ * record `ev_start` (a cudaEvent_t) immediately before and `ev_stop` immediately after the
+ * persistent beam kernel on the decode stream, so callers can time that kernel alone.
+ * Pass NULL, NULL to disable. */
+void flexctc_set_profile_events(void* ev_start, void* ev_stop);
+
 /* Reads the device flags of the last decode that used `workspace` (call after the stream has
  * synchronised). */
 flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags);

@@ -13,6 +13,8 @@
 namespace flexctc {
 
 thread_local std::string g_error;
+thread_local void* g_ev_start = nullptr;
+thread_local void* g_ev_stop = nullptr;
 void set_error(const std::string& msg) { g_error = msg; }
 flexctc_status fail(flexctc_status st, const std::string& msg) {
     g_error = msg;
@@ -300,10 +302,15 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
     p.out_tokens = out_tokens; p.out_num = out_num_tokens; p.out_scores = out_scores;
     p.out_ts = out_timestamps; p.out_align = out_alignment;
     std::string err;
-    int rc = launch_decode(p, (void*)stream, err);
+    int rc = launch_decode(p, (void*)stream, g_ev_start, g_ev_stop, err);
     if (rc == 2) return fail(FLEXCTC_ERR_CAPACITY, err);
     if (rc != 0) return fail(FLEXCTC_ERR_CUDA, err);
     return FLEXCTC_OK;
+}
+
+void flexctc_set_profile_events(void* ev_start, void* ev_stop) {
+    g_ev_start = ev_start;
+    g_ev_stop = ev_stop;
 }
 
 flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags) {

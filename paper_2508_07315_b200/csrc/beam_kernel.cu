@@ -687,7 +687,7 @@ size_t smem_bytes(int K, int Vp1, int R, int cap, int nch) {
 }
 
 template <int NT>
-int launch_nt(const DecodeParams& p, cudaStream_t st, std::string& err) {
+int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
     const int VP = (p.Vp1 + 3) & ~3;
     const int R = VP <= 2048 ? 4 : 2;
     const int cap = 8 * NT;
@@ -701,15 +701,17 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, std::string& err) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctc_beam_kernel<NT>, NT, sm);
     if (e != cudaSuccess || occ < 1) { err = "occupancy query failed"; return 1; }
     const int grid = std::min(p.B, nsm * occ);
+    if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
     ctc_beam_kernel<NT><<<grid, NT, sm, st>>>(p, R, cap);
     e = cudaGetLastError();
+    if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     return 0;
 }
 
 }  // namespace
 
-int launch_decode(const DecodeParams& p, void* stream, std::string& err) {
+int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std::string& err) {
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(p.flags, 0, 2 * sizeof(uint32_t), st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
@@ -719,10 +721,10 @@ int launch_decode(const DecodeParams& p, void* stream, std::string& err) {
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     const int nt = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
     switch (nt) {
-        case 32: return launch_nt<32>(p, st, err);
-        case 64: return launch_nt<64>(p, st, err);
-        case 128: return launch_nt<128>(p, st, err);
-        default: return launch_nt<256>(p, st, err);
+        case 32: return launch_nt<32>(p, st, ev0, ev1, err);
+        case 64: return launch_nt<64>(p, st, ev0, ev1, err);
+        case 128: return launch_nt<128>(p, st, ev0, ev1, err);
+        default: return launch_nt<256>(p, st, ev0, ev1, err);
     }
 }
 

@@ -108,7 +108,7 @@ struct WorkspaceLayout {
 WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K);
 
 // launches (beam_kernel.cu)
-int launch_decode(const DecodeParams& p, void* stream, std::string& err);
+int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
 
 }  // namespace flexctc
 

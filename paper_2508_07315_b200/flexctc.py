@@ -51,7 +51,7 @@ EXPORTS = [
     "flexctc_last_error", "flexctc_version", "flexctc_lm_load", "flexctc_lm_free", "flexctc_lm_get_info",
     "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
     "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
-    "flexctc_host_scratch_bytes", "flexctc_decode_host",
+    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_set_profile_events",
 ]
 
 
@@ -82,6 +82,8 @@ def _load() -> ctypes.CDLL:
     L.flexctc_host_scratch_bytes.argtypes = [i32, i32, i32, P(Config)]
     L.flexctc_host_scratch_bytes.restype = sz
     L.flexctc_decode_host.argtypes = [vp, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, vp, vp, vp, vp]
+    L.flexctc_set_profile_events.argtypes = [vp, vp]
+    L.flexctc_set_profile_events.restype = None
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if a declared symbol is missing
     return L
@@ -223,6 +225,12 @@ def decode(log_probs, lengths, cfg: Config, lm: LM | None = None, boost: Boost |
                                   _ptr(outputs["tokens"]), _ptr(outputs["num_tokens"]), _ptr(outputs["scores"]),
                                   _ptr(outputs.get("timestamps")), _ptr(outputs.get("alignment"))))
     return outputs
+
+
+def set_profile_events(start=None, stop=None):
+    """Record torch.cuda.Event `start`/`stop` around the beam kernel of later decode calls."""
+    lib.flexctc_set_profile_events(ctypes.c_void_p(start.cuda_event) if start is not None else None,
+                                   ctypes.c_void_p(stop.cuda_event) if stop is not None else None)
 
 
 def check(workspace: Workspace) -> int:

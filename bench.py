@@ -217,6 +217,9 @@ def run_flexctc(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for e in ev:  # torch creates events lazily: record once so the C hook gets real cudaEvent_t handles
+        e[2].record(stream)
+        e[3].record(stream)
 
     def step(e=None):
         nonlocal out

@@ -113,24 +113,30 @@ flexctc_status flexctc_lm_load(const char* arpa_path, int32_t vocab_size, const 
     if (device >= 0) {
         const LmHost& h = lm->host;
         Upload up;
-        size_t o_hdr = up.add(h.st_hdr.data(), h.st_hdr.size() * 4);
-        size_t o_tok = up.add(h.arc_tok.data(), h.arc_tok.size() * 2);
-        size_t o_val = up.add(h.arc_val.data(), h.arc_val.size() * 4);
+        if (h.NL > kMaxLmLevels) { delete lm; return fail(FLEXCTC_ERR_CAPACITY, "LM order > 8"); }
+        size_t o_rec = up.add(h.rec.data(), h.rec.size() * 4);
+        size_t o_den = up.add(h.dense.data(), h.dense.size() * 4);
+        std::vector<int32_t> arcs4(h.arc_tok.size() * 4, 0);
+        for (size_t k = 0; k < h.arc_tok.size(); ++k) {
+            arcs4[4 * k] = h.arc_tok[k];
+            arcs4[4 * k + 1] = h.arc_val[2 * k];
+            arcs4[4 * k + 2] = h.arc_val[2 * k + 1];
+        }
+        size_t o_arc = up.add(arcs4.data(), arcs4.size() * 4);
         size_t o_ulp = up.add(h.uni_lp.data(), h.uni_lp.size() * 4);
         size_t o_unx = up.add(h.uni_next.data(), h.uni_next.size() * 4);
-        size_t o_eos = up.add(h.eos.data(), h.eos.size() * 4);
-        size_t o_ub = up.add(h.ub.data(), h.ub.size() * 4);
         st = upload(device, up, &lm->dmem);
         if (st != FLEXCTC_OK) { delete lm; return st; }
         lm->dbytes = up.total();
         char* d = (char*)lm->dmem;
-        lm->dev.st_hdr = (const int4*)(d + o_hdr);
-        lm->dev.arc_tok = (const uint16_t*)(d + o_tok);
-        lm->dev.arc_val = (const int2*)(d + o_val);
+        lm->dev.rec = (const int4*)(d + o_rec);
+        lm->dev.dense = (const int2*)(d + o_den);
+        lm->dev.arcs = (const int4*)(d + o_arc);
         lm->dev.uni_lp = (const float*)(d + o_ulp);
         lm->dev.uni_next = (const int32_t*)(d + o_unx);
-        lm->dev.eos = (const float*)(d + o_eos);
-        lm->dev.ub = (const float*)(d + o_ub);
+        lm->dev.RW = h.RW;
+        lm->dev.V = h.V;
+        lm->dev.NL = h.NL;
         lm->dev.start = h.start;
     }
     *out = lm;

@@ -8,27 +8,32 @@
 //
 // B200 design:
 //  * one persistent CTA per in-flight utterance, utterances taken longest-first from a device
-//    work queue (LPT), the whole frame loop in-kernel: zero host syncs, one launch per decode;
-//  * frame rows D[b,t,:] streamed HBM -> shared memory with cp.async (16 B when aligned) in a
-//    ring R frames ahead of the recurrence, so the only O(B·T·V') HBM stream overlaps it;
-//  * exact pre-prune: the blank/repeat candidates (no fusion terms) give a lower bound mx0 of the
-//    frame max, hence τ0 = fl(mx0 - θ) <= τ; a non-blank candidate is scored exactly (LM arc
-//    search in L2 + boost table lookup) only if acc + D + ub(state) can reach τ0 (ub = β +
-//    α_LM·max_w P(w|lm) + α_BT·max_w delta(bt) + rounding margin). Everything below τ0 is pruned
-//    by Alg. 1 anyway, so the live beam is bit-identical to the dense [K, V'] evaluation;
+//    work queue (LPT); the whole frame loop runs in-kernel: zero host syncs, one launch;
+//  * frame rows D[b,t,:] stream HBM -> shared memory with cp.async (16 B when aligned) in a ring
+//    R frames ahead of the recurrence, so the only O(B·T·V') HBM stream overlaps it;
+//  * exact pre-prune. Lower bound of the frame max mx: the blank and repeat candidates (no fusion
+//    terms) and the exact candidates of the frame's best non-blank token from every live slot.
+//    τ0 = fl(mx0 - θ) <= τ. A non-blank candidate is scored exactly (LM + boost lookups) only if
+//    acc + D + ub(slot) can reach the running threshold (ub = β + α_LM·max_w P(w|lm state) +
+//    α_BT·max_w delta(bt state) + rounding margin). Anything below is pruned by Alg. 1 anyway or
+//    cannot enter the top K, so the live beam is bit-identical to the dense [K, V'] evaluation;
 //  * survivors go to a shared-memory buffer of 64-bit keys (orderable fp32 score | ~flat index);
 //    when it fills, a block radix-select keeps the top K and raises the threshold (threshold
-//    algorithm), so any candidate count (θ = ∞, flat frames) works in bounded memory;
-//  * selection = radix-select of the K-th key + rank sort of K keys; ties go to the lower flat
-//    index (reading R9) because the index is in the key;
-//  * recombination on (64-bit prefix hash, last label) (R12) over the K slots, log-sum-exp in the
-//    canonical order (R14) with exp/log1p evaluated in fp64 and rounded once;
-//  * backpointers u8 parent + u16 label per (t, k) in global memory plus per-32-frame chunk
-//    ancestors, so the backtrace walks chunks in parallel (T/32 + 32 dependent loads, not T).
+//    algorithm): any candidate count (θ = ∞, flat frames) works in bounded memory;
+//  * selection = radix-select of the K-th key + rank sort of <= K keys; ties go to the lower
+//    flat index (reading R9) because the index is in the key;
+//  * per-slot LM records (whole backoff chain, cumulative backoffs, bound, LM.Final) and boost
+//    values are cached in shared memory and carried with the slot, so an LM query is one round of
+//    parallel arc searches (all chain levels at once) plus one dense level-1 load;
+//  * recombination on (64-bit prefix hash, last label) (R12), log-sum-exp in the canonical order
+//    (R14) with exp/log1p evaluated in fp64 and rounded once;
+//  * backpointers u8 parent + u16 label per (t, k) plus per-32-frame chunk ancestors, so the
+//    backtrace walks chunks in parallel (T/32 + 32 dependent loads, not T).
 // All score arithmetic uses __fadd_rn/__fmaf_rn in the canonical order of reading R19 (no
 // contraction, no fast-math), so max-mode scores are bit-identical to the fp32 oracle.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -39,6 +44,7 @@ namespace flexctc {
 namespace {
 
 constexpr float kNeg = -INFINITY;
+constexpr int kRecMax = 8 + 3 * kMaxLmLevels + 2;  // ints per cached LM record (>= RW)
 
 __device__ __forceinline__ uint64_t hash_extend(uint64_t h, int w) {  // SPEC S:58 (FNV-64 prime)
     return (h ^ (uint64_t)(w + 1)) * 1099511628211ull;
@@ -50,59 +56,87 @@ __device__ __forceinline__ uint32_t ord_of(float s) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 __device__ __forceinline__ float score_of(uint64_t key) {
-    uint32_t o = (uint32_t)(key >> 32);
-    uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    const uint32_t o = (uint32_t)(key >> 32);
+    const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
     return __uint_as_float(u);
 }
 __device__ __forceinline__ uint64_t make_key(float s, uint32_t f) {
     return ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - f);
 }
 __device__ __forceinline__ uint32_t flat_of(uint64_t key) { return 0xffffffffu - (uint32_t)key; }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
 __device__ __forceinline__ void cp_async4(void* s, const void* g) {
-    uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
 }
 __device__ __forceinline__ void cp_async16(void* s, const void* g) {
-    uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// NGPU-LM query: log P(w | state) and the next state (walk the backoff chain; arcs are sorted by
-// token within a state). Same arithmetic order as lm_query_host and as the oracle (R19).
-__device__ __forceinline__ float lm_query(const LmDev& lm, int s, int w, int& next) {
-    float acc = 0.0f;
-    while (s != 0) {
-        const int4 h = __ldg(&lm.st_hdr[s]);
-        int lo = h.x, hi = h.x + h.y;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((int)__ldg(&lm.arc_tok[mid]) < w) lo = mid + 1; else hi = mid;
+// NGPU-LM query from a cached state record: log P(w | state) and the next state.
+// All arc levels (contexts of length >= 2) are binary-searched in lockstep (their loads are
+// independent), the level-1 dense row is loaded in parallel, and the first level holding w
+// wins; cum values are the fp32 backoff sums of the sequential walk (lm_query_host, R19).
+__device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict__ rec, int w, int& next) {
+    const int n = rec[0], u = rec[1];
+    int2 d = make_int2(0, 0);
+    if (u >= 0) d = __ldg(&lm.dense[(size_t)u * lm.V + w]);
+    int lo[kMaxLmLevels], hi[kMaxLmLevels], hit[kMaxLmLevels];
+#pragma unroll
+    for (int j = 0; j < kMaxLmLevels; ++j) {
+        lo[j] = j < n ? rec[8 + 3 * j] : 0;
+        hi[j] = j < n ? lo[j] + rec[8 + 3 * j + 1] : 0;
+        hit[j] = -1;
+    }
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < kMaxLmLevels; ++j) {
+            if (lo[j] < hi[j]) {
+                any = true;
+                const int mid = (lo[j] + hi[j]) >> 1;
+                const int t = __ldg(&lm.arcs[mid]).x;
+                if (t == w) { hit[j] = mid; hi[j] = lo[j]; }
+                else if (t < w) lo[j] = mid + 1;
+                else hi[j] = mid;
+            }
         }
-        if (lo < h.x + h.y && (int)__ldg(&lm.arc_tok[lo]) == w) {
-            const int2 v = __ldg(&lm.arc_val[lo]);
-            next = v.y;
-            return __fadd_rn(acc, __int_as_float(v.x));
+        if (!any) break;
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxLmLevels; ++j) {
+        if (hit[j] >= 0) {
+            const int4 a = __ldg(&lm.arcs[hit[j]]);
+            next = a.z;
+            return __fadd_rn(__int_as_float(rec[8 + 3 * j + 2]), __int_as_float(a.y));
         }
-        acc = __fadd_rn(acc, __int_as_float(h.w));
-        s = h.z;
+    }
+    if (u >= 0) {
+        const bool found = (d.y & 0x80000000) != 0;
+        next = d.y & 0x7fffffff;
+        return __fadd_rn(__int_as_float(found ? rec[2] : rec[3]), __int_as_float(d.x));
     }
     next = __ldg(&lm.uni_next[w]);
-    return __fadd_rn(acc, __ldg(&lm.uni_lp[w]));
+    return __fadd_rn(__int_as_float(rec[3]), __ldg(&lm.uni_lp[w]));
 }
+
+// one bank of per-slot state (two banks, swapped every frame)
+struct Bank {
+    float* acc; int* last; uint64_t* hash; int* lms; int* bts; uint8_t* anc;
+    int* rec;     // [K][RWS] cached LM record of lms
+    float* btm;   // [K][2]  {maxd, U} of bts
+};
 
 struct Shared {
     float* ring;
-    // current slot state
-    float* acc; int* last; uint64_t* hash; int* lms; int* bts; uint8_t* anc; float* ubv; float* uba;
-    // next slot state
-    float* acc2; int* last2; uint64_t* hash2; int* lms2; int* bts2; uint8_t* anc2;
-    // candidate buffer + selection
-    uint64_t* ckey; int* clm; int* cbt;
-    uint64_t* skey; int* slm; int* sbt;
+    Bank bk;  // bank 0; bank 1 of every field starts `K` (or K*stride) elements later
+    uint64_t* ckey; int* clm; int* cbt;   // candidate buffer [cap]
+    uint64_t* skey; int* slm; int* sbt;   // selection [K]
     uint16_t* toks;
     int* alive_idx;
     uint32_t* hist;
@@ -113,43 +147,80 @@ struct Scalars {
     int nbuf, m, nalive, nsel, u;
     float thr;
     uint64_t kth;
-    uint32_t prefix_found;
-    float red_f[32];
-    uint64_t red_k[32];
-    int red_i[32];
+    float rf[4][32];
+    uint64_t rk[32];
+    int ri[32];
 };
 
 template <int NT>
 __device__ __forceinline__ float block_max(float v, Scalars& sc) {
     constexpr int NW = NT / 32;
+#pragma unroll
     for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (NW == 1) return v;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     __syncthreads();
-    if (lane == 0) sc.red_f[wid] = v;
+    if (lane == 0) sc.rf[0][wid] = v;
     __syncthreads();
-    float r = sc.red_f[0];
+    float r = sc.rf[0][0];
 #pragma unroll
-    for (int i = 1; i < NW; ++i) r = fmaxf(r, sc.red_f[i]);
+    for (int i = 1; i < NW; ++i) r = fmaxf(r, sc.rf[0][i]);
     return r;
 }
 
 template <int NT>
 __device__ __forceinline__ uint64_t block_max_u64(uint64_t v, Scalars& sc) {
     constexpr int NW = NT / 32;
-    for (int o = 16; o; o >>= 1) {
-        uint64_t x = __shfl_xor_sync(0xffffffffu, v, o);
-        v = x > v ? x : v;
-    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (NW == 1) return v;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     __syncthreads();
-    if (lane == 0) sc.red_k[wid] = v;
+    if (lane == 0) sc.rk[wid] = v;
     __syncthreads();
-    uint64_t r = sc.red_k[0];
+    uint64_t r = sc.rk[0];
 #pragma unroll
-    for (int i = 1; i < NW; ++i) r = sc.red_k[i] > r ? sc.red_k[i] : r;
+    for (int i = 1; i < NW; ++i) r = umax64(r, sc.rk[i]);
     return r;
+}
+
+// Phase-1 reduction in one round: max of three floats, max of a u64 key, exclusive scan of a
+// 0/1 flag (slot order). Returns via references.
+template <int NT>
+__device__ __forceinline__ void block_reduce_p1(float& a, float& b, float& c, uint64_t& k, bool flag, int& off,
+                                                int& tot, Scalars& sc) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+        c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, o));
+        k = umax64(k, __shfl_xor_sync(0xffffffffu, k, o));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int in_warp = __popc(bal & ((1u << lane) - 1u));
+    if (NW == 1) {
+        off = in_warp;
+        tot = __popc(bal);
+        return;
+    }
+    __syncthreads();
+    if (lane == 0) {
+        sc.rf[0][wid] = a; sc.rf[1][wid] = b; sc.rf[2][wid] = c; sc.rk[wid] = k;
+        sc.ri[wid] = __popc(bal);
+    }
+    __syncthreads();
+    a = sc.rf[0][0]; b = sc.rf[1][0]; c = sc.rf[2][0]; k = sc.rk[0];
+    int base = 0, all = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        if (i) { a = fmaxf(a, sc.rf[0][i]); b = fmaxf(b, sc.rf[1][i]); c = fmaxf(c, sc.rf[2][i]); k = umax64(k, sc.rk[i]); }
+        if (i < wid) base += sc.ri[i];
+        all += sc.ri[i];
+    }
+    off = base + in_warp;
+    tot = all;
 }
 
 // exclusive prefix over the block of per-thread counts; returns the offset, total in *tot
@@ -158,25 +229,26 @@ __device__ __forceinline__ int block_exscan(int v, int* tot, Scalars& sc) {
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int x = v;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, x, o);
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
     __syncthreads();
-    if (lane == 31) sc.red_i[wid] = x;
+    if (lane == 31) sc.ri[wid] = x;
     __syncthreads();
     int base = 0, all = 0;
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
-        if (i < wid) base += sc.red_i[i];
-        all += sc.red_i[i];
+        if (i < wid) base += sc.ri[i];
+        all += sc.ri[i];
     }
     *tot = all;
     return base + x - v;
 }
 
-// Radix select over n unique 64-bit keys in smem: returns the key kth such that exactly K keys
-// are >= kth (n > K). MSB-first 8-bit digits; stops as soon as the boundary bin is exact.
+// Radix select over n unique 64-bit keys in smem: returns kth such that exactly K keys are
+// >= kth (requires n > K). MSB-first 8-bit digits; stops as soon as the boundary bin is exact.
 template <int NT>
 __device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Scalars& sc) {
     uint64_t prefix = 0, mask = 0;
@@ -190,27 +262,26 @@ __device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Sc
         }
         __syncthreads();
         if (threadIdx.x < 32) {
-            // lane l owns bins [248-8l .. 255-8l] (descending digits)
-            const int lane = threadIdx.x;
+            const int lane = threadIdx.x;  // lane l owns digits 255-8l .. 248-8l (descending)
             uint32_t c[8];
             uint32_t s = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) { c[j] = sm.hist[255 - 8 * lane - j]; s += c[j]; }
             uint32_t incl = s;
+#pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            uint32_t above = incl - s;  // keys in strictly higher digits than this lane's bins
+            const uint32_t above = incl - s;
             if (above < (uint32_t)remaining && (uint32_t)remaining <= incl) {
                 uint32_t a = above;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     if (a < (uint32_t)remaining && (uint32_t)remaining <= a + c[j]) {
-                        const uint32_t d = 255 - 8 * lane - j;
-                        sc.kth = (uint64_t)d;
-                        sc.red_i[0] = (int)((uint32_t)remaining - a);   // still needed inside bin d
-                        sc.red_i[1] = (int)c[j];                        // keys in bin d
+                        sc.kth = (uint64_t)(255 - 8 * lane - j);
+                        sc.ri[0] = (int)((uint32_t)remaining - a);
+                        sc.ri[1] = (int)c[j];
                     }
                     a += c[j];
                 }
@@ -218,14 +289,14 @@ __device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Sc
         }
         __syncthreads();
         const uint64_t d = sc.kth;
-        const int need = sc.red_i[0], inbin = sc.red_i[1];
+        const int need = sc.ri[0], inbin = sc.ri[1];
         __syncthreads();
         prefix |= d << shift;
         mask |= 255ull << shift;
         remaining = need;
-        if (need == inbin) return prefix;  // every key with this prefix is in: threshold = prefix
+        if (need == inbin) return prefix;
     }
-    return prefix;  // unique keys: the last digit pins the K-th key exactly
+    return prefix;
 }
 
 // Move the keys >= kth (exactly K of them) from the candidate buffer into the selection arrays.
@@ -243,6 +314,23 @@ __device__ void gather_selected(int n, uint64_t kth, Shared& sm, Scalars& sc) {
     __syncthreads();
 }
 
+__device__ __forceinline__ void push_cand(Shared& sm, Scalars& sc, uint64_t key, int lmn, int btn) {
+    const int j = atomicAdd(&sc.nbuf, 1);
+    sm.ckey[j] = key; sm.clm[j] = lmn; sm.cbt[j] = btn;
+}
+
+template <int NT>
+__device__ __forceinline__ void load_row(float* dst, const float* src, int Vp1) {
+    const int tid = threadIdx.x;
+    if ((((uintptr_t)src) & 15) == 0) {
+        const int n4 = Vp1 >> 2;
+        for (int i = tid; i < n4; i += NT) cp_async16(dst + 4 * i, src + 4 * i);
+        for (int i = 4 * n4 + tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
+    } else {
+        for (int i = tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
+    }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -251,18 +339,21 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
     const int K = p.K, Vp1 = p.Vp1, blank = Vp1 - 1;
     const int VP = (Vp1 + 3) & ~3;
     const int R = ring_rows;
+    const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
+    const int RWS = lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
+    const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
 
-    // ---- carve dynamic shared memory
     Shared sm;
     {
         unsigned char* q = smem_raw;
         auto take = [&](size_t bytes) { unsigned char* r = q; q += (bytes + 15) & ~size_t(15); return r; };
         sm.ring = (float*)take(sizeof(float) * (size_t)R * VP);
-        sm.acc = (float*)take(4 * K); sm.last = (int*)take(4 * K); sm.hash = (uint64_t*)take(8 * K);
-        sm.lms = (int*)take(4 * K); sm.bts = (int*)take(4 * K); sm.anc = (uint8_t*)take(K);
-        sm.ubv = (float*)take(4 * K); sm.uba = (float*)take(4 * K);
-        sm.acc2 = (float*)take(4 * K); sm.last2 = (int*)take(4 * K); sm.hash2 = (uint64_t*)take(8 * K);
-        sm.lms2 = (int*)take(4 * K); sm.bts2 = (int*)take(4 * K); sm.anc2 = (uint8_t*)take(K);
+        {
+            Bank& B = sm.bk;  // both banks of each field, contiguous
+            B.acc = (float*)take(8 * K); B.last = (int*)take(8 * K); B.hash = (uint64_t*)take(16 * K);
+            B.lms = (int*)take(8 * K); B.bts = (int*)take(8 * K); B.anc = (uint8_t*)take(2 * K);
+            B.rec = (int*)take(8 * (size_t)K * RWS); B.btm = (float*)take(16 * K);
+        }
         sm.ckey = (uint64_t*)take(8 * (size_t)cap); sm.clm = (int*)take(4 * (size_t)cap); sm.cbt = (int*)take(4 * (size_t)cap);
         sm.skey = (uint64_t*)take(8 * K); sm.slm = (int*)take(4 * K); sm.sbt = (int*)take(4 * K);
         sm.toks = (uint16_t*)take(2 * (size_t)Vp1);
@@ -270,8 +361,25 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
         sm.hist = (uint32_t*)take(4 * 256);
         sm.endslot = (int*)take(4 * (size_t)p.nch);
     }
-    const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
-    const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
+    auto bank = [&](int z) {
+        Bank B;
+        B.acc = sm.bk.acc + z * K; B.last = sm.bk.last + z * K; B.hash = sm.bk.hash + z * K;
+        B.lms = sm.bk.lms + z * K; B.bts = sm.bk.bts + z * K; B.anc = sm.bk.anc + z * K;
+        B.rec = sm.bk.rec + (size_t)z * K * RWS; B.btm = sm.bk.btm + z * 2 * K;
+        return B;
+    };
+
+    // exact candidate score of a non-blank, non-repeat token w from slot k (Eq. (1), R19 order)
+    auto eval = [&](const Bank& cur, int k, float s0, int w, int& ln, int& bn) -> float {
+        float s = __fadd_rn(s0, p.beta);
+        ln = cur.lms[k];
+        bn = cur.bts[k];
+        int2 e = make_int2(0, 0);
+        if (bt_on) e = __ldg(&p.bt.tab[(size_t)bn * p.bt.V + w]);               // issued first
+        if (lm_on) s = __fmaf_rn(p.alpha_lm, lm_query(p.lm, cur.rec + k * RWS, w, ln), s);
+        if (bt_on) { bn = e.x; s = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), s); }
+        return s;
+    };
 
     for (;;) {
         // ------------------------------------------------------------ next utterance (LPT queue)
@@ -285,49 +393,36 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
         const float* Db = p.log_probs + (int64_t)b * p.stride_b;
 
         // ------------------------------------------------------------ init (Alg. 1)
-        for (int k = tid; k < K; k += NT) {
-            sm.acc[k] = k == 0 ? 0.0f : kNeg;   // acc_scores[:,0] = 0, else -inf
-            sm.last[k] = blank;                  // R6
-            sm.hash[k] = 0ull;
-            sm.lms[k] = p.lm.start;              // LM(<SOS>)
-            sm.bts[k] = 0;                       // BT(<0>) = root
-            sm.anc[k] = 0;
-            float ub = p.beta, ua = fabsf(p.beta);
-            if (lm_on) { float x = p.alpha_lm * __ldg(&p.lm.ub[p.lm.start]); ub += x; ua += fabsf(x); }
-            sm.ubv[k] = ub_inf ? INFINITY : ub;
-            sm.uba[k] = ua;
-        }
-        // prologue: prefetch rows 0..R-2
-        for (int r = 0; r < R - 1; ++r) {
-            if (r < L) {
-                const float* src = Db + (int64_t)r * p.stride_t;
-                float* dst = sm.ring + (size_t)(r % R) * VP;
-                if ((((uintptr_t)src) & 15) == 0) {
-                    const int n4 = Vp1 >> 2;
-                    for (int i = tid; i < n4; i += NT) cp_async16(dst + 4 * i, src + 4 * i);
-                    for (int i = 4 * n4 + tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
-                } else {
-                    for (int i = tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
-                }
+        {
+            const Bank c0 = bank(0);
+            for (int k = tid; k < K; k += NT) {
+                c0.acc[k] = k == 0 ? 0.0f : kNeg;  // acc_scores[:,0] = 0, else -inf
+                c0.last[k] = blank;                 // R6
+                c0.hash[k] = 0ull;
+                c0.lms[k] = p.lm.start;             // LM(<SOS>)
+                c0.bts[k] = 0;                      // BT(<0>) = root
+                c0.anc[k] = 0;
             }
+            if (lm_on)
+                for (int i = tid; i < RWS / 4; i += NT)
+                    ((int4*)c0.rec)[i] = __ldg(&p.lm.rec[(size_t)p.lm.start * (p.lm.RW / 4) + i]);
+            if (tid == 0) {
+                c0.btm[0] = bt_on ? __ldg(&p.bt.maxd[0]) : 0.0f;
+                c0.btm[1] = bt_on ? __ldg(&p.bt.U[0]) : 0.0f;
+            }
+        }
+        for (int r = 0; r < R - 1; ++r) {  // prologue: rows 0..R-2
+            if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * VP, Db + (int64_t)r * p.stride_t, Vp1);
             cp_commit();
         }
 
+        int cb = 0;  // current bank
         for (int t = 0; t < L; ++t) {
-            // ---------------------------------------------------- stage row t (issue row t+R-1)
+            const Bank cur = bank(cb);
+            const Bank nxt = bank(cb ^ 1);
             {
                 const int r = t + R - 1;
-                if (r < L) {
-                    const float* src = Db + (int64_t)r * p.stride_t;
-                    float* dst = sm.ring + (size_t)(r % R) * VP;
-                    if ((((uintptr_t)src) & 15) == 0) {
-                        const int n4 = Vp1 >> 2;
-                        for (int i = tid; i < n4; i += NT) cp_async16(dst + 4 * i, src + 4 * i);
-                        for (int i = 4 * n4 + tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
-                    } else {
-                        for (int i = tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
-                    }
-                }
+                if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * VP, Db + (int64_t)r * p.stride_t, Vp1);
                 cp_commit();
             }
             if (R == 4) cp_wait<3>(); else cp_wait<1>();
@@ -335,113 +430,134 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             __syncthreads();
             const float* row = sm.ring + (size_t)(t % R) * VP;
 
-            // ---------------------------------------------------- phase 1: exact blank / repeat candidates
-            float a = kNeg, sbk = kNeg, srk = kNeg, ubk = kNeg;
+            // ------------------------------------------------ phase 1: exact blank/repeat candidates,
+            // per-slot bounds, frame argmax over non-blank tokens, alive list
+            float a = kNeg, sbk = kNeg, srk = kNeg, ubk = kNeg, uak = 0.0f;
             int lk = blank;
             bool al = false;
             if (tid < K) {
-                a = sm.acc[tid];
+                a = cur.acc[tid];
                 al = a > kNeg;
-                lk = sm.last[tid];
+                lk = cur.last[tid];
                 if (al) {
-                    sbk = __fadd_rn(a, row[blank]);            // blank: no β / fusion
-                    if (lk != blank) srk = __fadd_rn(a, row[lk]); // repeat: no β / fusion
-                    ubk = sm.ubv[tid];
+                    sbk = __fadd_rn(a, row[blank]);                 // blank: no β / fusion
+                    if (lk != blank) srk = __fadd_rn(a, row[lk]);    // repeat: no β / fusion
+                    float ub = p.beta, ua = fabsf(p.beta);
+                    if (lm_on) { const float x = p.alpha_lm * __int_as_float(cur.rec[tid * RWS + 4]); ub += x; ua += fabsf(x); }
+                    if (bt_on) { const float x = p.alpha_bt * cur.btm[2 * tid]; ub += x; ua += fabsf(x); }
+                    ubk = ub_inf ? INFINITY : ub;
+                    uak = ua;
                 }
             }
+            uint64_t best_tok = 0;
             {
-                // alive list (slot order)
-                const unsigned bal = __ballot_sync(0xffffffffu, al);
-                int tot;
-                const int off = block_exscan<NT>(al ? 1 : 0, &tot, sc);
-                if (al) sm.alive_idx[off] = tid;
-                (void)bal;
-                if (tid == 0) sc.nalive = tot;
+                float bv = kNeg;
+                int bi = -1;
+                for (int w = tid; w < blank; w += NT) {  // blank is the last index (R1)
+                    const float v = row[w];
+                    if (v > bv || bi < 0) { bv = v; bi = w; }
+                }
+                if (bi >= 0) best_tok = make_key(bv, (uint32_t)bi);
             }
-            const float mx0 = block_max<NT>(fmaxf(sbk, srk), sc);
-            const float accmax = block_max<NT>(a, sc);
-            const float ubvmax = block_max<NT>(ubk, sc);
-            const float tau0 = __fsub_rn(mx0, p.theta);   // lower bound of fl(max - θ)
-            if (tid == 0) sc.thr = tau0;
+            float mxrb = fmaxf(sbk, srk), accmax = a, ubvmax = ubk;
+            int aoff, nalive;
+            block_reduce_p1<NT>(mxrb, accmax, ubvmax, best_tok, al, aoff, nalive, sc);
+            if (al) sm.alive_idx[aoff] = tid;
+            const int wstar = (int)flat_of(best_tok);
+            const float dstar = score_of(best_tok);
             __syncthreads();
-            if (al) {
-                if (sbk > kNeg && sbk >= tau0) {
-                    const int j = atomicAdd(&sc.nbuf, 1);
-                    sm.ckey[j] = make_key(sbk, (uint32_t)(tid * Vp1 + blank));
-                    sm.clm[j] = sm.lms[tid]; sm.cbt[j] = sm.bts[tid];
-                }
-                if (srk > kNeg && srk >= tau0) {
-                    const int j = atomicAdd(&sc.nbuf, 1);
-                    sm.ckey[j] = make_key(srk, (uint32_t)(tid * Vp1 + lk));
-                    sm.clm[j] = sm.lms[tid]; sm.cbt[j] = sm.bts[tid];
-                }
+
+            // ------------------------------------------------ phase 2: exact candidates of the frame's
+            // best non-blank token (tightens the lower bound of the frame max on emission frames)
+            bool stage_a = false;
+            float tau0 = __fsub_rn(mxrb, p.theta);
+            if (nalive > 0 && mxrb > kNeg) {
+                const float reach = __fadd_rn(__fadd_rn(accmax, dstar), ubvmax) +
+                                    1e-4f * (1.0f + fabsf(accmax) + fabsf(dstar) + fabsf(ubvmax));
+                stage_a = reach >= mxrb;
             }
-            // ---------------------------------------------------- phase 2: frame token filter
-            // any non-rb candidate that can reach tau0 has D[w] >= tau0 - accmax - ubvmax - margin
-            if (mx0 > kNeg) {
+            float sA = kNeg;
+            int lnA = 0, bnA = 0, kA = -1;
+            if (stage_a) {
+                if (tid < nalive) {
+                    kA = sm.alive_idx[tid];
+                    if (wstar != cur.last[kA]) sA = eval(cur, kA, __fadd_rn(cur.acc[kA], dstar), wstar, lnA, bnA);
+                }
+                const float mxA = block_max<NT>(sA, sc);
+                tau0 = __fsub_rn(fmaxf(mxrb, mxA), p.theta);  // lower bound of fl(max - θ)
+            }
+            if (al) {
+                if (sbk > kNeg && sbk >= tau0) push_cand(sm, sc, make_key(sbk, (uint32_t)(tid * Vp1 + blank)), cur.lms[tid], cur.bts[tid]);
+                if (srk > kNeg && srk >= tau0) push_cand(sm, sc, make_key(srk, (uint32_t)(tid * Vp1 + lk)), cur.lms[tid], cur.bts[tid]);
+            }
+            if (sA > kNeg && sA >= tau0) push_cand(sm, sc, make_key(sA, (uint32_t)(kA * Vp1 + wstar)), lnA, bnA);
+
+            // ------------------------------------------------ phase 3: frame token filter
+            // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
+            if (nalive > 0 && mxrb > kNeg) {
                 const float mg = 1e-4f * (1.0f + fabsf(tau0) + fabsf(accmax) + fabsf(ubvmax));
                 const float dthr = __fsub_rn(__fsub_rn(__fsub_rn(tau0, accmax), ubvmax), mg);
-                for (int w0 = 0; w0 < Vp1; w0 += NT) {
-                    const int w = w0 + tid;
-                    const bool hit = w < Vp1 && w != blank && row[w] >= dthr;
-                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                    if (bal) {
-                        int base = 0;
-                        if ((tid & 31) == 0) base = atomicAdd(&sc.m, __popc(bal));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (hit) sm.toks[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = (uint16_t)w;
+                const bool maybe = stage_a ? true : (dstar >= dthr);
+                if (maybe) {
+                    for (int w0 = 0; w0 < Vp1; w0 += NT) {
+                        const int w = w0 + tid;
+                        const bool hit = w < Vp1 && w != blank && !(stage_a && w == wstar) && row[w] >= dthr;
+                        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                        if (bal) {
+                            int base = 0;
+                            if ((tid & 31) == 0) base = atomicAdd(&sc.m, __popc(bal));
+                            base = __shfl_sync(0xffffffffu, base, 0);
+                            if (hit) sm.toks[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = (uint16_t)w;
+                        }
                     }
                 }
             }
+            if (tid == 0) sc.thr = tau0;
             __syncthreads();
-            // ---------------------------------------------------- phase 3: exact non-rb candidates
+
+            // ------------------------------------------------ phase 4: exact non-rb candidates
             {
                 const int m = sc.m;
-                const int npairs = sc.nalive * m;
-                for (int base = 0; base < npairs; base += NT) {
-                    if (sc.nbuf > cap - NT) {
-                        // buffer full: keep the top K, raise the threshold (threshold algorithm)
-                        const int n = sc.nbuf;
-                        const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
-                        gather_selected<NT>(n, kth, sm, sc);
-                        for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
-                        if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); }
-                        __syncthreads();
-                    }
-                    const float thr = sc.thr;
-                    const int pi = base + tid;
-                    if (pi < npairs) {
-                        const int k = sm.alive_idx[pi / m];
-                        const int w = sm.toks[pi % m];
-                        if (w != sm.last[k]) {
-                            const float ak = sm.acc[k];
-                            const float s0 = __fadd_rn(ak, row[w]);
-                            const float uv = sm.ubv[k];
-                            const float bound = __fadd_rn(s0, uv) + 1e-5f * (1.0f + fabsf(s0) + sm.uba[k]);
-                            if (bound >= thr) {
-                                float s = __fadd_rn(s0, p.beta);
-                                int ln = sm.lms[k], bn = sm.bts[k];
-                                if (lm_on) {
-                                    const float lp = lm_query(p.lm, ln, w, ln);
-                                    s = __fmaf_rn(p.alpha_lm, lp, s);
-                                }
-                                if (bt_on) {
-                                    const int2 e = __ldg(&p.bt.tab[(size_t)bn * p.bt.V + w]);
-                                    bn = e.x;
-                                    s = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), s);
-                                }
-                                if (s > kNeg && s >= thr) {
-                                    const int j = atomicAdd(&sc.nbuf, 1);
-                                    sm.ckey[j] = make_key(s, (uint32_t)(k * Vp1 + w));
-                                    sm.clm[j] = ln; sm.cbt[j] = bn;
+                if (m > 0) {
+                    int lp = 0;
+                    while ((1 << lp) < nalive) ++lp;
+                    const int per = NT >> lp;  // tokens per pass
+                    for (int base = 0; base < m; base += per) {
+                        if (sc.nbuf > cap - NT) {
+                            // buffer full: keep the top K, raise the threshold (threshold algorithm)
+                            const int n = sc.nbuf;
+                            const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
+                            gather_selected<NT>(n, kth, sm, sc);
+                            for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
+                            if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); }
+                            __syncthreads();
+                        }
+                        const float thr = sc.thr;
+                        const int ai = tid & ((1 << lp) - 1);
+                        const int j = base + (tid >> lp);
+                        if (ai < nalive && j < m) {
+                            const int k = sm.alive_idx[ai];
+                            const int w = sm.toks[j];
+                            if (w != cur.last[k]) {
+                                const float s0 = __fadd_rn(cur.acc[k], row[w]);
+                                float ub = p.beta, ua = fabsf(p.beta);
+                                if (lm_on) { const float x = p.alpha_lm * __int_as_float(cur.rec[k * RWS + 4]); ub += x; ua += fabsf(x); }
+                                if (bt_on) { const float x = p.alpha_bt * cur.btm[2 * k]; ub += x; ua += fabsf(x); }
+                                if (ub_inf) ub = INFINITY;
+                                const float bound = __fadd_rn(s0, ub) + 1e-5f * (1.0f + fabsf(s0) + ua);
+                                if (bound >= thr) {
+                                    int ln, bn;
+                                    const float s = eval(cur, k, s0, w, ln, bn);
+                                    if (s > kNeg && s >= thr) push_cand(sm, sc, make_key(s, (uint32_t)(k * Vp1 + w)), ln, bn);
                                 }
                             }
                         }
+                        __syncthreads();
                     }
-                    __syncthreads();
                 }
             }
-            // ---------------------------------------------------- phase 4: flat TopK + θ-prune
+
+            // ------------------------------------------------ phase 5: flat TopK + θ-prune
             const int n = sc.nbuf;
             const uint64_t* kk;
             const int* kl;
@@ -454,7 +570,6 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             } else {
                 kk = sm.ckey; kl = sm.clm; kb = sm.cbt; nsel = n;
             }
-            // rank sort (keys are unique); entry -> slot rank when rank < K
             uint64_t myk = 0;
             int rank = 0, myl = 0, myb = 0;
             if (tid < nsel) {
@@ -465,61 +580,73 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             if (tid < nsel && rank < K) { sm.skey[rank] = myk; sm.slm[rank] = myl; sm.sbt[rank] = myb; }
             __syncthreads();
             const int nkeep = nsel < K ? nsel : K;
-            const float mx = nkeep > 0 ? score_of(sm.skey[0]) : kNeg;   // max_score
-            const float tau = __fsub_rn(mx, p.theta);                        // P:139
-            // ---------------------------------------------------- phase 5: beams.update
+            const float mx = nkeep > 0 ? score_of(sm.skey[0]) : kNeg;  // max_score
+            const float tau = __fsub_rn(mx, p.theta);                      // P:139
+
+            // ------------------------------------------------ phase 6: beams.update into nxt
             const int64_t bpo = ((int64_t)b * p.T + t) * K;
+            bool live = false, emit = false;
+            int par = 0;
+            int4 rec_ld[kRecMax / 4];
+            float2 bt_ld = make_float2(0.0f, 0.0f);
             if (tid < K) {
                 const int i = tid;
-                bool live = false;
                 if (i < nkeep) {
                     const uint64_t key = sm.skey[i];
                     const float s = score_of(key);
                     if (s >= tau) {
                         live = true;
                         const uint32_t f = flat_of(key);
-                        const int par = (int)(f / (uint32_t)Vp1), w = (int)(f % (uint32_t)Vp1);
-                        const int pl = sm.last[par];
-                        const bool emit = w != blank && w != pl;
-                        sm.acc2[i] = s;
-                        sm.last2[i] = w;
-                        sm.hash2[i] = emit ? hash_extend(sm.hash[par], w) : sm.hash[par];
-                        sm.lms2[i] = sm.slm[i];   // rb candidates carry the parent's states
-                        sm.bts2[i] = sm.sbt[i];
-                        sm.anc2[i] = (t % kChunk == 0) ? (uint8_t)par : sm.anc[par];
+                        par = (int)(f / (uint32_t)Vp1);
+                        const int w = (int)(f % (uint32_t)Vp1);
+                        emit = w != blank && w != cur.last[par];
+                        const int ln = sm.slm[i], bn = sm.sbt[i];
+                        if (emit) {  // new LM / BT states: fetch their records (latency overlaps phase 7)
+                            if (lm_on)
+#pragma unroll
+                                for (int q = 0; q < kRecMax / 4; ++q)
+                                    if (4 * q < RWS) rec_ld[q] = __ldg(&p.lm.rec[(size_t)ln * (p.lm.RW / 4) + q]);
+                            if (bt_on) bt_ld = make_float2(__ldg(&p.bt.maxd[bn]), __ldg(&p.bt.U[bn]));
+                        }
+                        nxt.acc[i] = s;
+                        nxt.last[i] = w;
+                        nxt.hash[i] = emit ? hash_extend(cur.hash[par], w) : cur.hash[par];
+                        nxt.lms[i] = ln;  // rb candidates carry the parent's states
+                        nxt.bts[i] = bn;
+                        nxt.anc[i] = (t % kChunk == 0) ? (uint8_t)par : cur.anc[par];
                         p.bp_parent[bpo + i] = (uint8_t)par;
                         p.bp_label[bpo + i] = (uint16_t)w;
                     }
                 }
                 if (!live) {
-                    sm.acc2[i] = kNeg;
-                    sm.last2[i] = blank;
-                    sm.hash2[i] = 0ull;
-                    sm.lms2[i] = 0; sm.bts2[i] = 0; sm.anc2[i] = 0;
+                    nxt.acc[i] = kNeg;
+                    nxt.last[i] = blank;
+                    nxt.hash[i] = 0ull;
+                    nxt.lms[i] = 0; nxt.bts[i] = 0; nxt.anc[i] = 0;
                     p.bp_parent[bpo + i] = 0xff;
                     p.bp_label[bpo + i] = 0xffff;
                 }
             }
             __syncthreads();
-            // ---------------------------------------------------- phase 6: RecombineHypotheses
+            // ------------------------------------------------ phase 7: RecombineHypotheses
             if (tid < K) {
                 const int i = tid;
-                float s = sm.acc2[i];
+                float s = nxt.acc[i];
                 if (s > kNeg) {
-                    const uint64_t h = sm.hash2[i];
-                    const int l = sm.last2[i];
+                    const uint64_t h = nxt.hash[i];
+                    const int l = nxt.last[i];
                     bool dead = false;
                     for (int j = 0; j < i; ++j)
-                        if (sm.acc2[j] > kNeg && sm.hash2[j] == h && sm.last2[j] == l) { dead = true; break; }
+                        if (nxt.acc[j] > kNeg && nxt.hash[j] == h && nxt.last[j] == l) { dead = true; break; }
                     if (dead) {
                         s = kNeg;
                     } else {
-                        // slots are in (score desc, flat asc) order, so the group order is slot order
+                        // slots are in (score desc, flat asc) order, so group order == slot order
                         float sum = 0.0f;
                         bool any = false;
                         for (int j = i + 1; j < K; ++j) {
-                            const float sj = sm.acc2[j];
-                            if (sj > kNeg && sm.hash2[j] == h && sm.last2[j] == l) {
+                            const float sj = nxt.acc[j];
+                            if (sj > kNeg && nxt.hash[j] == h && nxt.last[j] == l) {
                                 any = true;
                                 if (p.merge_mode == 0) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(sj, s)));
                             }
@@ -527,71 +654,79 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
                         if (any && p.merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
                     }
                 }
-                sm.acc[i] = s;
-                sm.last[i] = sm.last2[i];
-                sm.hash[i] = sm.hash2[i];
-                sm.lms[i] = sm.lms2[i];
-                sm.bts[i] = sm.bts2[i];
-                sm.anc[i] = sm.anc2[i];
-                if (s > kNeg) {
-                    float ub = p.beta, ua = fabsf(p.beta);
-                    if (lm_on) { float x = p.alpha_lm * __ldg(&p.lm.ub[sm.lms2[i]]); ub += x; ua += fabsf(x); }
-                    if (bt_on) { float x = p.alpha_bt * __ldg(&p.bt.maxd[sm.bts2[i]]); ub += x; ua += fabsf(x); }
-                    sm.ubv[i] = ub_inf ? INFINITY : ub;
-                    sm.uba[i] = ua;
-                }
                 if ((t % kChunk) == kChunk - 1 || t == L - 1)
-                    p.chunk_anc[((int64_t)b * p.nch + t / kChunk) * K + i] = sm.anc2[i];
+                    p.chunk_anc[((int64_t)b * p.nch + t / kChunk) * K + i] = nxt.anc[i];
+                // cached records of the new slot states
+                if (live) {
+                    if (emit) {
+                        if (lm_on)
+#pragma unroll
+                            for (int q = 0; q < kRecMax / 4; ++q)
+                                if (4 * q < RWS) ((int4*)(nxt.rec + i * RWS))[q] = rec_ld[q];
+                        nxt.btm[2 * i] = bt_ld.x;
+                        nxt.btm[2 * i + 1] = bt_ld.y;
+                    } else {
+                        if (lm_on)
+                            for (int q = 0; q < RWS / 4; ++q)
+                                ((int4*)(nxt.rec + i * RWS))[q] = ((const int4*)(cur.rec + par * RWS))[q];
+                        nxt.btm[2 * i] = cur.btm[2 * par];
+                        nxt.btm[2 * i + 1] = cur.btm[2 * par + 1];
+                    }
+                }
+                sm.skey[i] = (uint64_t)__float_as_uint(s);  // stash merged score
             }
+            __syncthreads();
+            if (tid < K) nxt.acc[tid] = __uint_as_float((uint32_t)sm.skey[tid]);
+            cb ^= 1;
             __syncthreads();
         }
         cp_wait<0>();
+        const Bank cur = bank(cb);
 
         // ------------------------------------------------------------ EOS + final merge (R15)
+        float fs = kNeg;
         if (tid < K) {
-            float s = sm.acc[tid];
-            if (s > kNeg) {
-                if (lm_on) s = __fmaf_rn(p.alpha_lm, __ldg(&p.lm.eos[sm.lms[tid]]), s);
-                if (bt_on && p.retract) s = __fmaf_rn(-p.alpha_bt, __ldg(&p.bt.U[sm.bts[tid]]), s);
+            fs = cur.acc[tid];
+            if (fs > kNeg) {
+                if (lm_on) fs = __fmaf_rn(p.alpha_lm, __int_as_float(cur.rec[tid * RWS + 5]), fs);
+                if (bt_on && p.retract) fs = __fmaf_rn(-p.alpha_bt, cur.btm[2 * tid + 1], fs);
             }
-            sm.acc2[tid] = s;
+            sm.skey[tid] = (uint64_t)__float_as_uint(fs);
         }
         __syncthreads();
         uint64_t bestkey = 0;
-        if (tid < K) {
+        if (tid < K && fs > kNeg) {
             const int i = tid;
-            float s = sm.acc2[i];
-            if (s > kNeg) {
-                const uint64_t h = sm.hash[i];
-                bool dead = false;
-                for (int j = 0; j < K; ++j) {
-                    const float sj = sm.acc2[j];
-                    if (j != i && sj > kNeg && sm.hash[j] == h && (sj > s || (sj == s && j < i))) { dead = true; break; }
-                }
-                if (!dead) {
-                    // other members in (score desc, slot asc) order
-                    float sum = 0.0f;
-                    bool any = false;
-                    float prev_s = INFINITY;
-                    int prev_j = -1;
-                    for (;;) {
-                        int bj = -1;
-                        float bs = kNeg;
-                        for (int j = 0; j < K; ++j) {
-                            const float sj = sm.acc2[j];
-                            if (j == i || !(sj > kNeg) || sm.hash[j] != h) continue;
-                            const bool after_prev = sj < prev_s || (sj == prev_s && j > prev_j);
-                            if (!after_prev) continue;
-                            if (bj < 0 || sj > bs || (sj == bs && j < bj)) { bj = j; bs = sj; }
-                        }
-                        if (bj < 0) break;
-                        any = true;
-                        if (p.merge_mode == 0) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(bs, s)));
-                        prev_s = bs; prev_j = bj;
+            float s = fs;
+            const uint64_t h = cur.hash[i];
+            auto sc_of = [&](int j) { return __uint_as_float((uint32_t)sm.skey[j]); };
+            bool dead = false;
+            for (int j = 0; j < K; ++j) {
+                const float sj = sc_of(j);
+                if (j != i && sj > kNeg && cur.hash[j] == h && (sj > s || (sj == s && j < i))) { dead = true; break; }
+            }
+            if (!dead) {
+                float sum = 0.0f;
+                bool any = false;
+                float prev_s = INFINITY;
+                int prev_j = -1;
+                for (;;) {  // other members in (score desc, slot asc) order
+                    int bj = -1;
+                    float bs = kNeg;
+                    for (int j = 0; j < K; ++j) {
+                        const float sj = sc_of(j);
+                        if (j == i || !(sj > kNeg) || cur.hash[j] != h) continue;
+                        if (!(sj < prev_s || (sj == prev_s && j > prev_j))) continue;
+                        if (bj < 0 || sj > bs || (sj == bs && j < bj)) { bj = j; bs = sj; }
                     }
-                    if (any && p.merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
-                    bestkey = ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - (uint32_t)i);
+                    if (bj < 0) break;
+                    any = true;
+                    if (p.merge_mode == 0) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(bs, s)));
+                    prev_s = bs;
+                    prev_j = bj;
                 }
+                if (any && p.merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
+                bestkey = ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - (uint32_t)i);
             }
         }
         bestkey = block_max_u64<NT>(bestkey, sc);
@@ -675,11 +810,11 @@ __global__ void order_kernel(const int32_t* __restrict__ lengths, int B, int T, 
     order[rank] = b;
 }
 
-size_t smem_bytes(int K, int Vp1, int R, int cap, int nch) {
+size_t smem_bytes(int K, int Vp1, int R, int cap, int nch, int RWS) {
     const int VP = (Vp1 + 3) & ~3;
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
     size_t s = al(sizeof(float) * (size_t)R * VP);
-    s += 2 * (al(4 * K) + al(4 * K) + al(8 * K) + al(4 * K) + al(4 * K) + al(K)) + 2 * al(4 * K);
+    s += al(8 * K) + al(8 * K) + al(16 * K) + al(8 * K) + al(8 * K) + al(2 * K) + al(8 * (size_t)K * RWS) + al(16 * K);
     s += al(8 * (size_t)cap) + 2 * al(4 * (size_t)cap);
     s += al(8 * K) + 2 * al(4 * K);
     s += al(2 * (size_t)Vp1) + al(4 * K) + al(4 * 256) + al(4 * (size_t)nch);
@@ -691,7 +826,8 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std:
     const int VP = (p.Vp1 + 3) & ~3;
     const int R = VP <= 2048 ? 4 : 2;
     const int cap = 8 * NT;
-    const size_t sm = smem_bytes(p.K, p.Vp1, R, cap, p.nch);
+    const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
+    const size_t sm = smem_bytes(p.K, p.Vp1, R, cap, p.nch, RWS);
     if (sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
     cudaError_t e = cudaFuncSetAttribute(ctc_beam_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }

@@ -22,26 +22,32 @@ flexctc_status fail(flexctc_status st, const std::string& msg);
 //   per state     eos[S] = LM.Final and lm_ub[S] >= max_w log P(w | s) (pre-prune bound)
 // State 0 is the root (empty context); it has no CSR arcs (the dense row replaces them).
 // ---------------------------------------------------------------------------------------
+// Device query structures derived from it:
+//   rec[S][RW]    per-state record: {n_arc_levels, dense_row(-1 = none), cum_u, cum_root, ub, eos,
+//                 0, 0, then per arc level (context length >= 2): arc_off, arc_deg, cum}
+//   dense[U][V]   rows of the length-1 contexts: {f32 value, next | found_at_level1 << 31}
 struct LmHost {
     int32_t order = 0, V = 0, S = 0, start = 0;
+    int32_t NL = 0, RW = 8, U = 0;
     std::vector<int32_t> st_hdr;   // 4 ints per state
     std::vector<uint16_t> arc_tok;
     std::vector<int32_t> arc_val;  // 2 ints per arc: f32 bits, next
     std::vector<float> uni_lp;
     std::vector<int32_t> uni_next;
     std::vector<float> eos, ub;
+    std::vector<int32_t> rec;      // S * RW
+    std::vector<int32_t> dense;    // U * V * 2
 };
 
 struct LmDev {
-    const int4* st_hdr;
-    const uint16_t* arc_tok;
-    const int2* arc_val;
+    const int4* rec;               // S * RW/4 int4
+    const int2* dense;
+    const int4* arcs;              // {token, f32 logp bits, next state, 0}, sorted per state
     const float* uni_lp;
     const int32_t* uni_next;
-    const float* eos;
-    const float* ub;
-    int32_t start;
+    int32_t RW, V, start, NL;
 };
+constexpr int kMaxLmLevels = 6;    // arc levels (order - 2); order <= 8
 
 // ---------------------------------------------------------------------------------------
 // Boost device layout: full Aho-Corasick transition table [nodes x V] of {next, f32 delta}

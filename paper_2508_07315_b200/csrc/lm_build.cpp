@@ -300,31 +300,100 @@ flexctc_status build_lm_host(const char* path, int32_t V, const char* const* sym
         for (int32_t s = 0; s < S; ++s) out.ub[s] = (float)(ub[s] + 1e-5 * (1.0 + std::fabs(ub[s])));
     }
     out.start = (BOS >= 0 && N >= 2) ? longest_state_suffix(&BOS, 1) : 0;
+
+    // ---- device query structures:
+    // per-state record = the whole backoff chain unrolled: arc levels (contexts of length >= 2:
+    // CSR offset, degree, and the fp32 backoff sum accumulated when the sequential walk reaches
+    // that level), the length-1 context (index of its dense row) with its accumulated sum, the
+    // sum at the root, the pre-prune bound and LM.Final. All levels can then be searched in
+    // parallel and the first level holding the token wins — bit-identical to the sequential walk.
+    out.NL = std::max(0, N - 2);
+    out.RW = ((8 + 3 * out.NL) + 3) & ~3;
+    std::vector<int32_t> dense_idx(S, -1);
+    int32_t U = 0;
+    for (int32_t s = 1; s < S; ++s)
+        if (st_len[s] == 1) dense_idx[s] = U++;
+    out.U = U;
+    out.rec.assign((size_t)S * out.RW, 0);
+    for (int32_t s = 0; s < S; ++s) {
+        int32_t* r = &out.rec[(size_t)s * out.RW];
+        float acc = 0.0f, cum_u = 0.0f;
+        int32_t x = s, n = 0, u = -1;
+        while (x != 0) {
+            if (st_len[x] >= 2) {
+                const int32_t* h = &out.st_hdr[(size_t)x * 4];
+                r[8 + 3 * n] = h[0];
+                r[8 + 3 * n + 1] = h[1];
+                memcpy(&r[8 + 3 * n + 2], &acc, 4);
+                ++n;
+            } else {
+                u = dense_idx[x];
+                cum_u = acc;
+            }
+            acc = acc + st_bw[x];
+            x = st_bo[x];
+        }
+        r[0] = n;
+        r[1] = u;
+        memcpy(&r[2], &cum_u, 4);
+        memcpy(&r[3], &acc, 4);
+        memcpy(&r[4], &out.ub[s], 4);
+        memcpy(&r[5], &out.eos[s], 4);
+    }
+    // dense rows of the length-1 contexts: {value, next | found<<31} for every decoder token
+    out.dense.assign((size_t)U * V * 2, 0);
+    for (int32_t s = 1; s < S; ++s) {
+        if (dense_idx[s] < 0) continue;
+        const int32_t* h = &out.st_hdr[(size_t)s * 4];
+        int32_t* row = &out.dense[(size_t)dense_idx[s] * V * 2];
+        for (int w = 0; w < V; ++w) {
+            float v = out.uni_lp[w];
+            int32_t nx = out.uni_next[w];
+            const uint16_t* b = out.arc_tok.data() + h[0];
+            const uint16_t* e = b + h[1];
+            const uint16_t* it = std::lower_bound(b, e, (uint16_t)w);
+            if (it != e && *it == (uint16_t)w) {
+                size_t k = (size_t)(it - out.arc_tok.data());
+                memcpy(&v, &out.arc_val[2 * k], 4);
+                nx = out.arc_val[2 * k + 1] | (int32_t)0x80000000u;
+            }
+            memcpy(&row[2 * w], &v, 4);
+            row[2 * w + 1] = nx;
+        }
+    }
     return FLEXCTC_OK;
 }
 
-// Host mirror of the device query (beam_kernel.cu lm_query): identical arithmetic order.
+// Host mirror of the device query (beam_kernel.cu lm_query): the same record walk, the same
+// fp32 operations in the same order.
 float lm_query_host(const LmHost& lm, int32_t s, int32_t w, int32_t* next) {
-    float acc = 0.0f;
-    while (s != 0) {
-        const int32_t* h = &lm.st_hdr[(size_t)s * 4];
-        const uint16_t* b = lm.arc_tok.data() + h[0];
-        const uint16_t* e = b + h[1];
+    const int32_t* r = &lm.rec[(size_t)s * lm.RW];
+    for (int j = 0; j < r[0]; ++j) {
+        const uint16_t* b = lm.arc_tok.data() + r[8 + 3 * j];
+        const uint16_t* e = b + r[8 + 3 * j + 1];
         const uint16_t* it = std::lower_bound(b, e, (uint16_t)w);
         if (it != e && *it == (uint16_t)w) {
             size_t k = (size_t)(it - lm.arc_tok.data());
-            float lp;
+            float lp, cum;
             memcpy(&lp, &lm.arc_val[2 * k], 4);
+            memcpy(&cum, &r[8 + 3 * j + 2], 4);
             *next = lm.arc_val[2 * k + 1];
-            return acc + lp;
+            return cum + lp;
         }
-        float bw;
-        memcpy(&bw, &h[3], 4);
-        acc = acc + bw;
-        s = h[2];
+    }
+    float cum_u, cum_root;
+    memcpy(&cum_u, &r[2], 4);
+    memcpy(&cum_root, &r[3], 4);
+    if (r[1] >= 0) {
+        const int32_t* d = &lm.dense[((size_t)r[1] * lm.V + w) * 2];
+        float v;
+        memcpy(&v, &d[0], 4);
+        const bool found = (d[1] & (int32_t)0x80000000u) != 0;
+        *next = d[1] & 0x7fffffff;
+        return (found ? cum_u : cum_root) + v;
     }
     *next = lm.uni_next[w];
-    return acc + lm.uni_lp[w];
+    return cum_root + lm.uni_lp[w];
 }
 
 }  // namespace flexctc

@@ -251,6 +251,7 @@ def run_flexctc(args):
     t_dec = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3        # s, whole decode per step summed
     t_kern = sum(e[2].elapsed_time(e[3]) for e in ev) / 1e3       # s, beam kernel only
     flags = F.check(ws)
+    dstats = FX.stats(ws)  # device counters of the last timed decode
     tt = torch.tensor([t_dec, t_kern], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -322,6 +323,7 @@ def run_flexctc(args):
             "clocks": clk,
             "e2e": e2e,
             "device_flags": flags,
+            "device_stats_per_step": dstats,
         }
         if gathered is not None:
             res["gathered_tokens"] = gathered

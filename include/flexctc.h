@@ -154,6 +154,12 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
  * Pass NULL, NULL to disable. */
 void flexctc_set_profile_events(void* ev_start, void* ev_stop);
 
+/* Device counters of the last decode that used `workspace` (call after the stream has
+ * synchronised); copies min(n, 16) u64 values: frames, sum of live slots, sum of listed tokens,
+ * sparse exact evaluations, dense frames, LM rows built, dense exact evaluations, buffer
+ * compactions, top-token stages, deferred next-state queries. */
+flexctc_status flexctc_get_stats(const void* workspace, uint64_t* out, int32_t n);
+
 /* Reads the device flags of the last decode that used `workspace` (call after the stream has
  * synchronised). */
 flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags);

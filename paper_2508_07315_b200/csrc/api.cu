@@ -81,7 +81,7 @@ WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K) {
     w.nch = (T + kChunk - 1) / kChunk;
     if (w.nch < 1) w.nch = 1;
     size_t o = 0;
-    w.flags = o; o += align256(16);
+    w.flags = o; o += align256(64 + 8 * kStatsWords);
     w.order = o; o += align256(4 * (size_t)B);
     w.len_c = o; o += align256(4 * (size_t)B);
     w.chunk_anc = o; o += align256((size_t)B * w.nch * K);
@@ -298,6 +298,7 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
     if (boost) p.bt = boost->dev;
     char* w = (char*)workspace;
     p.flags = (uint32_t*)(w + wl.flags);
+    p.stats = (unsigned long long*)(w + wl.flags + 64);
     p.order = (int32_t*)(w + wl.order);
     p.len_c = (int32_t*)(w + wl.len_c);
     p.chunk_anc = (uint8_t*)(w + wl.chunk_anc);
@@ -317,6 +318,14 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
 void flexctc_set_profile_events(void* ev_start, void* ev_stop) {
     g_ev_start = ev_start;
     g_ev_stop = ev_stop;
+}
+
+flexctc_status flexctc_get_stats(const void* workspace, uint64_t* out, int32_t n) {
+    if (!workspace || !out || n < 0) return fail(FLEXCTC_ERR_INVALID_ARG, "bad argument");
+    const int k = n < kStatsWords ? n : kStatsWords;
+    cudaError_t e = cudaMemcpy(out, (const char*)workspace + 64, 8 * (size_t)k, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy");
+    return FLEXCTC_OK;
 }
 
 flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags) {

@@ -44,7 +44,7 @@ namespace flexctc {
 namespace {
 
 constexpr float kNeg = -INFINITY;
-constexpr int kRecMax = 8 + 3 * kMaxLmLevels + 2;  // ints per cached LM record (>= RW)
+constexpr int kDenseMinTokens = 24;                 // listed tokens per frame that switch to LM rows
 
 __device__ __forceinline__ uint64_t hash_extend(uint64_t h, int w) {  // SPEC S:58 (FNV-64 prime)
     return (h ^ (uint64_t)(w + 1)) * 1099511628211ull;
@@ -82,13 +82,14 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // All arc levels (contexts of length >= 2) are binary-searched in lockstep (their loads are
 // independent), the level-1 dense row is loaded in parallel, and the first level holding w
 // wins; cum values are the fp32 backoff sums of the sequential walk (lm_query_host, R19).
+template <int LMV>  // max arc levels (order - 2)
 __device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict__ rec, int w, int& next) {
     const int n = rec[0], u = rec[1];
     int2 d = make_int2(0, 0);
     if (u >= 0) d = __ldg(&lm.dense[(size_t)u * lm.V + w]);
-    int lo[kMaxLmLevels], hi[kMaxLmLevels], hit[kMaxLmLevels];
+    int lo[LMV], hi[LMV], hit[LMV];
 #pragma unroll
-    for (int j = 0; j < kMaxLmLevels; ++j) {
+    for (int j = 0; j < LMV; ++j) {
         lo[j] = j < n ? rec[8 + 3 * j] : 0;
         hi[j] = j < n ? lo[j] + rec[8 + 3 * j + 1] : 0;
         hit[j] = -1;
@@ -96,7 +97,7 @@ __device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict
     for (;;) {
         bool any = false;
 #pragma unroll
-        for (int j = 0; j < kMaxLmLevels; ++j) {
+        for (int j = 0; j < LMV; ++j) {
             if (lo[j] < hi[j]) {
                 any = true;
                 const int mid = (lo[j] + hi[j]) >> 1;
@@ -109,7 +110,7 @@ __device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict
         if (!any) break;
     }
 #pragma unroll
-    for (int j = 0; j < kMaxLmLevels; ++j) {
+    for (int j = 0; j < LMV; ++j) {
         if (hit[j] >= 0) {
             const int4 a = __ldg(&lm.arcs[hit[j]]);
             next = a.z;
@@ -331,19 +332,62 @@ __device__ __forceinline__ void load_row(float* dst, const float* src, int Vp1) 
     }
 }
 
+// Fill an LM row: row[w] = log P(w | state) for every decoder token w, in exactly the fp32
+// arithmetic of lm_query (dense level-1 path first, then arc levels from the shortest context to
+// the longest so the longest listed context wins). Coalesced reads of the level-1 table.
 template <int NT>
-__global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap) {
+__device__ void build_lm_row(const LmDev& lm, int state, float* row, int V) {
+    const int4* r4 = lm.rec + (size_t)state * (lm.RW / 4);
+    const int4 h0 = __ldg(&r4[0]);
+    const int n = h0.x, u = h0.y;
+    const float cum_u = __int_as_float(h0.z), cum_root = __int_as_float(h0.w);
+    if (u >= 0) {
+        const int2* d = lm.dense + (size_t)u * V;
+        for (int w = threadIdx.x; w < V; w += NT) {
+            const int2 e = __ldg(&d[w]);
+            row[w] = __fadd_rn((e.y & 0x80000000) ? cum_u : cum_root, __int_as_float(e.x));
+        }
+    } else {
+        for (int w = threadIdx.x; w < V; w += NT) row[w] = __fadd_rn(cum_root, __ldg(&lm.uni_lp[w]));
+    }
+    const int* ri = (const int*)r4;
+    for (int j = n - 1; j >= 0; --j) {
+        __syncthreads();
+        const int off = __ldg(&ri[8 + 3 * j]), deg = __ldg(&ri[8 + 3 * j + 1]);
+        const float cum = __int_as_float(__ldg(&ri[8 + 3 * j + 2]));
+        for (int a = threadIdx.x; a < deg; a += NT) {
+            const int4 arc = __ldg(&lm.arcs[off + a]);
+            row[arc.x] = __fadd_rn(cum, __int_as_float(arc.y));
+        }
+    }
+}
+
+// per-CTA device counters (SURVEY §5 "device counters"), flushed per utterance
+enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEvalDense, kCompactions,
+            kStageA, kDeferredNext, kNumStats };
+
+template <int NT, int LMV>
+__global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
+                                                      const int nrow) {
+    constexpr int kRec = (8 + 3 * LMV + 3) & ~3;  // ints per cached LM record
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Scalars sc;
+    __shared__ int s_line[kMaxBeam];       // per alive position: row-cache line (-1 = sparse path)
+    __shared__ int s_build[2 * 32];        // rows to build: (line, state)
+    __shared__ int s_nbuild;
     const int tid = threadIdx.x;
-    const int K = p.K, Vp1 = p.Vp1, blank = Vp1 - 1;
+    const int K = p.K, Vp1 = p.Vp1, blank = Vp1 - 1, V = Vp1 - 1;
     const int VP = (Vp1 + 3) & ~3;
     const int R = ring_rows;
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
     const int RWS = lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
+    uint32_t st[kNumStats] = {};
 
     Shared sm;
+    float* rowval = nullptr;  // [nrow][VP] LM rows (row cache)
+    int* rowtag = nullptr;    // [nrow] LM state of each line (-1 = empty)
+    int2* btroot = nullptr;   // [V] boost transition row of the root {next, delta}
     {
         unsigned char* q = smem_raw;
         auto take = [&](size_t bytes) { unsigned char* r = q; q += (bytes + 15) & ~size_t(15); return r; };
@@ -360,7 +404,15 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
         sm.alive_idx = (int*)take(4 * K);
         sm.hist = (uint32_t*)take(4 * 256);
         sm.endslot = (int*)take(4 * (size_t)p.nch);
+        if (nrow > 0) {
+            rowval = (float*)take(4 * (size_t)nrow * VP);
+            rowtag = (int*)take(4 * (size_t)nrow);
+        }
+        if (bt_on) btroot = (int2*)take(8 * (size_t)V);
     }
+    for (int i = tid; i < nrow; i += NT) rowtag[i] = -1;
+    if (bt_on)
+        for (int w = tid; w < V; w += NT) btroot[w] = __ldg(&p.bt.tab[w]);
     auto bank = [&](int z) {
         Bank B;
         B.acc = sm.bk.acc + z * K; B.last = sm.bk.last + z * K; B.hash = sm.bk.hash + z * K;
@@ -370,14 +422,21 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
     };
 
     // exact candidate score of a non-blank, non-repeat token w from slot k (Eq. (1), R19 order)
-    auto eval = [&](const Bank& cur, int k, float s0, int w, int& ln, int& bn) -> float {
+    // With `row` (a cached LM row of the slot's state) the LM value comes from shared memory and
+    // the next LM state is deferred (ln = -1) until the candidate is selected.
+    auto eval = [&](const Bank& cur, int k, float s0, int w, int& ln, int& bn, const float* row) -> float {
         float s = __fadd_rn(s0, p.beta);
         ln = cur.lms[k];
         bn = cur.bts[k];
         int2 e = make_int2(0, 0);
-        if (bt_on) e = __ldg(&p.bt.tab[(size_t)bn * p.bt.V + w]);               // issued first
-        if (lm_on) s = __fmaf_rn(p.alpha_lm, lm_query(p.lm, cur.rec + k * RWS, w, ln), s);
-        if (bt_on) { bn = e.x; s = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), s); }         // P:131
+        if (bt_on) e = bn == 0 ? btroot[w] : __ldg(&p.bt.tab[(size_t)bn * V + w]);  // issued first
+        if (lm_on) {
+            float lp;
+            if (row) { lp = row[w]; ln = -1; }
+            else lp = lm_query<LMV>(p.lm, cur.rec + k * RWS, w, ln);
+            s = __fmaf_rn(p.alpha_lm, lp, s);
+        }
+        if (bt_on) { bn = e.x; s = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), s); }  // P:131
         return s;
     };
 
@@ -481,7 +540,7 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             if (stage_a) {
                 if (tid < nalive) {
                     kA = sm.alive_idx[tid];
-                    if (wstar != cur.last[kA]) sA = eval(cur, kA, __fadd_rn(cur.acc[kA], dstar), wstar, lnA, bnA);
+                    if (wstar != cur.last[kA]) sA = eval(cur, kA, __fadd_rn(cur.acc[kA], dstar), wstar, lnA, bnA, nullptr);
                 }
                 const float mxA = block_max<NT>(sA, sc);
                 tau0 = __fsub_rn(fmaxf(mxrb, mxA), p.theta);  // lower bound of fl(max - θ)
@@ -518,6 +577,41 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             // ------------------------------------------------ phase 4: exact non-rb candidates
             {
                 const int m = sc.m;
+                if (tid == 0) {
+                    st[kFrames] += 1; st[kAlive] += nalive; st[kListed] += m; st[kStageA] += stage_a ? 1 : 0;
+                }
+                // dense frame: many listed tokens. Score them from LM rows cached in shared memory
+                // (the paper's full-vocabulary NGPU-LM query) instead of per-pair arc searches.
+                const bool dense = lm_on && nrow > 0 && m >= kDenseMinTokens;
+                if (dense) {
+                    if (tid == 0) {
+                        int nb = 0;
+                        unsigned used = 0;  // lines referenced this frame (nrow <= 32)
+                        for (int a2 = 0; a2 < nalive; ++a2) {
+                            const int st_ = cur.lms[sm.alive_idx[a2]];
+                            int line = -1;
+                            for (int l = 0; l < nrow; ++l)
+                                if (rowtag[l] == st_) { line = l; break; }
+                            if (line < 0) {
+                                for (int l = 0; l < nrow; ++l)
+                                    if (!(used >> l & 1u)) { line = l; break; }
+                                if (line >= 0) { rowtag[line] = st_; s_build[2 * nb] = line; s_build[2 * nb + 1] = st_; ++nb; }
+                            }
+                            if (line >= 0) used |= 1u << line;
+                            s_line[a2] = line;
+                        }
+                        s_nbuild = nb;
+                        st[kDenseFrames] += 1;
+                        st[kRowsBuilt] += nb;
+                    }
+                    __syncthreads();
+                    for (int i = 0; i < s_nbuild; ++i)
+                        build_lm_row<NT>(p.lm, s_build[2 * i + 1], rowval + (size_t)s_build[2 * i] * VP, V);
+                    __syncthreads();
+                } else if (m > 0) {
+                    for (int a2 = tid; a2 < nalive; a2 += NT) s_line[a2] = -1;
+                    __syncthreads();
+                }
                 if (m > 0) {
                     int lp = 0;
                     while ((1 << lp) < nalive) ++lp;
@@ -529,7 +623,7 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
                             const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
                             gather_selected<NT>(n, kth, sm, sc);
                             for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
-                            if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); }
+                            if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); st[kCompactions] += 1; }
                             __syncthreads();
                         }
                         const float thr = sc.thr;
@@ -540,14 +634,22 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
                             const int w = sm.toks[j];
                             if (w != cur.last[k]) {
                                 const float s0 = __fadd_rn(cur.acc[k], row[w]);
+                                const int line = s_line[ai];
                                 float ub = p.beta, ua = fabsf(p.beta);
-                                if (lm_on) { const float x = p.alpha_lm * __int_as_float(cur.rec[k * RWS + 4]); ub += x; ua += fabsf(x); }
+                                if (lm_on) {
+                                    // cached row: exact LM value for the bound; else the state's max
+                                    const float lmb = line >= 0 ? rowval[(size_t)line * VP + w]
+                                                                : __int_as_float(cur.rec[k * RWS + 4]);
+                                    const float x = p.alpha_lm * lmb;
+                                    ub += x; ua += fabsf(x);
+                                }
                                 if (bt_on) { const float x = p.alpha_bt * cur.btm[2 * k]; ub += x; ua += fabsf(x); }
                                 if (ub_inf) ub = INFINITY;
                                 const float bound = __fadd_rn(s0, ub) + 1e-5f * (1.0f + fabsf(s0) + ua);
                                 if (bound >= thr) {
                                     int ln, bn;
-                                    const float s = eval(cur, k, s0, w, ln, bn);
+                                    const float s = eval(cur, k, s0, w, ln, bn, line >= 0 ? rowval + (size_t)line * VP : nullptr);
+                                    st[line >= 0 ? kEvalDense : kEvalSparse] += 1;
                                     if (s > kNeg && s >= thr) push_cand(sm, sc, make_key(s, (uint32_t)(k * Vp1 + w)), ln, bn);
                                 }
                             }
@@ -587,7 +689,7 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             const int64_t bpo = ((int64_t)b * p.T + t) * K;
             bool live = false, emit = false;
             int par = 0;
-            int4 rec_ld[kRecMax / 4];
+            int4 rec_ld[kRec / 4];
             float2 bt_ld = make_float2(0.0f, 0.0f);
             if (tid < K) {
                 const int i = tid;
@@ -600,11 +702,16 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
                         par = (int)(f / (uint32_t)Vp1);
                         const int w = (int)(f % (uint32_t)Vp1);
                         emit = w != blank && w != cur.last[par];
-                        const int ln = sm.slm[i], bn = sm.sbt[i];
+                        int ln = sm.slm[i];
+                        const int bn = sm.sbt[i];
+                        if (emit && ln < 0) {  // scored from a cached row: resolve the next LM state now
+                            lm_query<LMV>(p.lm, cur.rec + par * RWS, w, ln);
+                            st[kDeferredNext] += 1;
+                        }
                         if (emit) {  // new LM / BT states: fetch their records (latency overlaps phase 7)
                             if (lm_on)
 #pragma unroll
-                                for (int q = 0; q < kRecMax / 4; ++q)
+                                for (int q = 0; q < kRec / 4; ++q)
                                     if (4 * q < RWS) rec_ld[q] = __ldg(&p.lm.rec[(size_t)ln * (p.lm.RW / 4) + q]);
                             if (bt_on) bt_ld = make_float2(__ldg(&p.bt.maxd[bn]), __ldg(&p.bt.U[bn]));
                         }
@@ -629,10 +736,34 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             }
             __syncthreads();
             // ------------------------------------------------ phase 7: RecombineHypotheses
+            unsigned grp = 0;
+            if constexpr (NT == 32) {
+                // one warp holds the beam: group lanes by (hash, last) with match.any
+                const bool lv = tid < K && nxt.acc[tid] > kNeg;
+                const uint64_t hk = lv ? nxt.hash[tid] : (0xfedcba9800000000ull | (uint64_t)tid);
+                const int lkey = lv ? nxt.last[tid] : -1 - tid;
+                const unsigned livemask = __ballot_sync(0xffffffffu, lv);
+                grp = __match_any_sync(0xffffffffu, hk) & __match_any_sync(0xffffffffu, lkey) & livemask;
+            }
             if (tid < K) {
                 const int i = tid;
                 float s = nxt.acc[i];
-                if (s > kNeg) {
+                if (NT == 32 && s > kNeg) {
+                    if (grp & ((1u << i) - 1u)) {
+                        s = kNeg;  // a better (lower) slot of the group survives
+                    } else {
+                        unsigned others = grp & ~((2u << i) - 1u);  // higher slots, ascending order
+                        if (others && p.merge_mode == 0) {
+                            float sum = 0.0f;
+                            while (others) {
+                                const int j = __ffs(others) - 1;
+                                others &= others - 1u;
+                                sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(nxt.acc[j], s)));
+                            }
+                            s = __fadd_rn(s, (float)log1p((double)sum));
+                        }
+                    }
+                } else if (s > kNeg) {
                     const uint64_t h = nxt.hash[i];
                     const int l = nxt.last[i];
                     bool dead = false;
@@ -661,7 +792,7 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
                     if (emit) {
                         if (lm_on)
 #pragma unroll
-                            for (int q = 0; q < kRecMax / 4; ++q)
+                            for (int q = 0; q < kRec / 4; ++q)
                                 if (4 * q < RWS) ((int4*)(nxt.rec + i * RWS))[q] = rec_ld[q];
                         nxt.btm[2 * i] = bt_ld.x;
                         nxt.btm[2 * i + 1] = bt_ld.y;
@@ -788,6 +919,9 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             p.out_scores[b] = best_score;
         }
     }
+#pragma unroll
+    for (int i = 0; i < kNumStats; ++i)
+        if (st[i]) atomicAdd(&p.stats[i], (unsigned long long)st[i]);
 }
 
 // Clamp lengths, flag anomalies, and order utterances longest-first (LPT) for the work queue.
@@ -821,24 +955,33 @@ size_t smem_bytes(int K, int Vp1, int R, int cap, int nch, int RWS) {
     return s;
 }
 
-template <int NT>
+template <int NT, int LMV>
 int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
     const int VP = (p.Vp1 + 3) & ~3;
     const int R = VP <= 2048 ? 4 : 2;
     const int cap = 8 * NT;
     const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
-    const size_t sm = smem_bytes(p.K, p.Vp1, R, cap, p.nch, RWS);
+    size_t sm = smem_bytes(p.K, p.Vp1, R, cap, p.nch, RWS) + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) + 16 : 0);
     if (sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
-    cudaError_t e = cudaFuncSetAttribute(ctc_beam_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    // LM row cache: as many lines as fit a ~110 KB CTA (2 CTAs / SM), at most min(K, 32)
+    int nrow = 0;
+    if (p.use_lm) {
+        const size_t line = 4 * (size_t)VP + 4;
+        const size_t budget = 110 * 1024;
+        if (sm + 16 < budget) nrow = (int)std::min<size_t>((budget - sm - 16) / line, (size_t)std::min(p.K, 32));
+        sm += nrow ? 4 * (size_t)nrow * VP + ((4 * (size_t)nrow + 15) & ~size_t(15)) : 0;
+    }
+    auto kern = ctc_beam_kernel<NT, LMV>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     int dev = 0, nsm = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctc_beam_kernel<NT>, NT, sm);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm);
     if (e != cudaSuccess || occ < 1) { err = "occupancy query failed"; return 1; }
     const int grid = std::min(p.B, nsm * occ);
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-    ctc_beam_kernel<NT><<<grid, NT, sm, st>>>(p, R, cap);
+    kern<<<grid, NT, sm, st>>>(p, R, cap, nrow);
     e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
@@ -849,18 +992,19 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std:
 
 int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std::string& err) {
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(p.flags, 0, 2 * sizeof(uint32_t), st);
+    cudaError_t e = cudaMemsetAsync(p.flags, 0, 64 + 8 * kStatsWords, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     if (p.B == 0) return 0;
     order_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p.lengths, p.B, p.T, p.order, p.len_c, p.flags, p.B <= 16384);
     e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     const int nt = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
+    const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
     switch (nt) {
-        case 32: return launch_nt<32>(p, st, ev0, ev1, err);
-        case 64: return launch_nt<64>(p, st, ev0, ev1, err);
-        case 128: return launch_nt<128>(p, st, ev0, ev1, err);
-        default: return launch_nt<256>(p, st, ev0, ev1, err);
+        case 32: return small_lm ? launch_nt<32, 2>(p, st, ev0, ev1, err) : launch_nt<32, kMaxLmLevels>(p, st, ev0, ev1, err);
+        case 64: return small_lm ? launch_nt<64, 2>(p, st, ev0, ev1, err) : launch_nt<64, kMaxLmLevels>(p, st, ev0, ev1, err);
+        case 128: return small_lm ? launch_nt<128, 2>(p, st, ev0, ev1, err) : launch_nt<128, kMaxLmLevels>(p, st, ev0, ev1, err);
+        default: return small_lm ? launch_nt<256, 2>(p, st, ev0, ev1, err) : launch_nt<256, kMaxLmLevels>(p, st, ev0, ev1, err);
     }
 }
 

@@ -51,8 +51,10 @@ EXPORTS = [
     "flexctc_last_error", "flexctc_version", "flexctc_lm_load", "flexctc_lm_free", "flexctc_lm_get_info",
     "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
     "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
-    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_set_profile_events",
+    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_set_profile_events", "flexctc_get_stats",
 ]
+STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
+              "exact_dense", "compactions", "top_token_stages", "deferred_next"]
 
 
 def _load() -> ctypes.CDLL:
@@ -84,6 +86,7 @@ def _load() -> ctypes.CDLL:
     L.flexctc_decode_host.argtypes = [vp, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, vp, vp, vp, vp]
     L.flexctc_set_profile_events.argtypes = [vp, vp]
     L.flexctc_set_profile_events.restype = None
+    L.flexctc_get_stats.argtypes = [vp, vp, i32]
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if a declared symbol is missing
     return L
@@ -231,6 +234,13 @@ def set_profile_events(start=None, stop=None):
     """Record torch.cuda.Event `start`/`stop` around the beam kernel of later decode calls."""
     lib.flexctc_set_profile_events(ctypes.c_void_p(start.cuda_event) if start is not None else None,
                                    ctypes.c_void_p(stop.cuda_event) if stop is not None else None)
+
+
+def stats(workspace: Workspace) -> dict:
+    """Device counters of the last decode on `workspace` (after the stream has synchronised)."""
+    out = np.zeros(len(STAT_NAMES), dtype=np.uint64)
+    _check(lib.flexctc_get_stats(_ptr(workspace.buf), out.ctypes.data_as(ctypes.c_void_p), len(STAT_NAMES)))
+    return {k: int(v) for k, v in zip(STAT_NAMES, out)}
 
 
 def check(workspace: Workspace) -> int:

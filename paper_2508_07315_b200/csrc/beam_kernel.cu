@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "flexctc_internal.h"
@@ -320,16 +321,22 @@ __device__ __forceinline__ void push_cand(Shared& sm, Scalars& sc, uint64_t key,
     sm.ckey[j] = key; sm.clm[j] = lmn; sm.cbt[j] = btn;
 }
 
+// A ring slot holds one frame row at float offset row_off(src) (0..3) so that shared and global
+// addresses agree mod 16 B: every row, aligned or not (4100-B rows at V' = 1025), is copied with
+// 16-B cp.async except for <= 3 head and tail elements.
+__device__ __forceinline__ int row_off(const float* src) { return (int)(((uintptr_t)src >> 2) & 3); }
+
 template <int NT>
-__device__ __forceinline__ void load_row(float* dst, const float* src, int Vp1) {
+__device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1) {
     const int tid = threadIdx.x;
-    if ((((uintptr_t)src) & 15) == 0) {
-        const int n4 = Vp1 >> 2;
-        for (int i = tid; i < n4; i += NT) cp_async16(dst + 4 * i, src + 4 * i);
-        for (int i = 4 * n4 + tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
-    } else {
-        for (int i = tid; i < Vp1; i += NT) cp_async4(dst + i, src + i);
-    }
+    const int off = row_off(src);
+    float* dst = slot + off;
+    const int h = min((4 - off) & 3, Vp1);
+    if (tid < h) cp_async4(dst + tid, src + tid);
+    const int n4 = (Vp1 - h) >> 2;
+    for (int i = tid; i < n4; i += NT) cp_async16(dst + h + 4 * i, src + h + 4 * i);
+    const int t0 = h + 4 * n4;
+    if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
 }
 
 // Fill an LM row: row[w] = log P(w | state) for every decoder token w, in exactly the fp32
@@ -367,12 +374,14 @@ enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEv
             kStageA, kDeferredNext, kNumStats };
 
 template <int NT, int LMV>
-__global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
+__global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
                                                       const int nrow) {
     constexpr int kRec = (8 + 3 * LMV + 3) & ~3;  // ints per cached LM record
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Scalars sc;
     __shared__ int s_line[kMaxBeam];       // per alive position: row-cache line (-1 = sparse path)
+    __shared__ float4 s_pos[kMaxBeam];     // per alive position: {acc, ub, |ub terms|, last}
+    __shared__ float s_ubnl[kMaxBeam];     // per alive position: ub without the LM term
     __shared__ int s_build[2 * 32];        // rows to build: (line, state)
     __shared__ int s_nbuild;
     const int tid = threadIdx.x;
@@ -391,7 +400,7 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
     {
         unsigned char* q = smem_raw;
         auto take = [&](size_t bytes) { unsigned char* r = q; q += (bytes + 15) & ~size_t(15); return r; };
-        sm.ring = (float*)take(sizeof(float) * (size_t)R * VP);
+        sm.ring = (float*)take(sizeof(float) * (size_t)R * (VP + 4));
         {
             Bank& B = sm.bk;  // both banks of each field, contiguous
             B.acc = (float*)take(8 * K); B.last = (int*)take(8 * K); B.hash = (uint64_t*)take(16 * K);
@@ -471,7 +480,7 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             }
         }
         for (int r = 0; r < R - 1; ++r) {  // prologue: rows 0..R-2
-            if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * VP, Db + (int64_t)r * p.stride_t, Vp1);
+            if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1);
             cp_commit();
         }
 
@@ -481,13 +490,13 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
             const Bank nxt = bank(cb ^ 1);
             {
                 const int r = t + R - 1;
-                if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * VP, Db + (int64_t)r * p.stride_t, Vp1);
+                if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1);
                 cp_commit();
             }
             if (R == 4) cp_wait<3>(); else cp_wait<1>();
             if (tid == 0) { sc.nbuf = 0; sc.m = 0; }
             __syncthreads();
-            const float* row = sm.ring + (size_t)(t % R) * VP;
+            const float* row = sm.ring + (size_t)(t % R) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
 
             // ------------------------------------------------ phase 1: exact blank/repeat candidates,
             // per-slot bounds, frame argmax over non-blank tokens, alive list
@@ -610,51 +619,68 @@ __global__ void __launch_bounds__(NT) ctc_beam_kernel(const DecodeParams p, cons
                     __syncthreads();
                 } else if (m > 0) {
                     for (int a2 = tid; a2 < nalive; a2 += NT) s_line[a2] = -1;
-                    __syncthreads();
                 }
                 if (m > 0) {
-                    int lp = 0;
-                    while ((1 << lp) < nalive) ++lp;
-                    const int per = NT >> lp;  // tokens per pass
-                    for (int base = 0; base < m; base += per) {
-                        if (sc.nbuf > cap - NT) {
-                            // buffer full: keep the top K, raise the threshold (threshold algorithm)
-                            const int n = sc.nbuf;
-                            const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
-                            gather_selected<NT>(n, kth, sm, sc);
-                            for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
-                            if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); st[kCompactions] += 1; }
-                            __syncthreads();
-                        }
-                        const float thr = sc.thr;
-                        const int ai = tid & ((1 << lp) - 1);
-                        const int j = base + (tid >> lp);
-                        if (ai < nalive && j < m) {
-                            const int k = sm.alive_idx[ai];
-                            const int w = sm.toks[j];
-                            if (w != cur.last[k]) {
-                                const float s0 = __fadd_rn(cur.acc[k], row[w]);
-                                const int line = s_line[ai];
-                                float ub = p.beta, ua = fabsf(p.beta);
-                                if (lm_on) {
-                                    // cached row: exact LM value for the bound; else the state's max
-                                    const float lmb = line >= 0 ? rowval[(size_t)line * VP + w]
-                                                                : __int_as_float(cur.rec[k * RWS + 4]);
-                                    const float x = p.alpha_lm * lmb;
-                                    ub += x; ua += fabsf(x);
+                    // per live position: {acc, ub (β + α_LM·max P + α_BT·max Δ), |terms|, last}
+                    for (int a2 = tid; a2 < nalive; a2 += NT) {
+                        const int k = sm.alive_idx[a2];
+                        float ub = p.beta, ua = fabsf(p.beta), ubnl = p.beta;
+                        if (lm_on) { const float x = p.alpha_lm * __int_as_float(cur.rec[k * RWS + 4]); ub += x; ua += fabsf(x); }
+                        if (bt_on) { const float x = p.alpha_bt * cur.btm[2 * k]; ub += x; ua += fabsf(x); ubnl += x; }
+                        if (ub_inf) { ub = INFINITY; ubnl = INFINITY; }
+                        s_pos[a2] = make_float4(cur.acc[k], ub, ua, __int_as_float(cur.last[k]));
+                        s_ubnl[a2] = ubnl;
+                    }
+                    __syncthreads();
+                    // token-major: lane = listed token, loop over the live slots. A lane whose push
+                    // would overflow the buffer records where it stopped; the block compacts the
+                    // buffer (top K, raised threshold) and the lane resumes there (no duplicates).
+                    for (int base = 0; base < m; base += NT) {
+                        const int j = base + tid;
+                        const int w = j < m ? (int)sm.toks[j] : -1;
+                        const float dw = w >= 0 ? row[w] : 0.0f;
+                        int a_from = w >= 0 ? 0 : nalive;
+                        for (;;) {
+                            if (sc.nbuf > cap - NT) {
+                                // buffer full: keep the top K, raise the threshold (threshold algorithm)
+                                const int n = sc.nbuf;
+                                const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
+                                gather_selected<NT>(n, kth, sm, sc);
+                                for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
+                                if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); st[kCompactions] += 1; }
+                                __syncthreads();
+                            }
+                            const float thr = sc.thr;
+                            bool ovf = false;
+                            for (int a2 = a_from; a2 < nalive; ++a2) {
+                                const float4 ps = s_pos[a2];
+                                if (w == __float_as_int(ps.w)) continue;  // repeat: scored in phase 1
+                                const float s0 = __fadd_rn(ps.x, dw);
+                                if (__fadd_rn(s0, ps.y) + 1e-5f * (1.0f + fabsf(s0) + ps.z) < thr) continue;
+                                const int k = sm.alive_idx[a2];
+                                const int line = s_line[a2];
+                                const float* lrow = line >= 0 ? rowval + (size_t)line * VP : nullptr;
+                                if (lrow) {  // exact LM value from the cached row tightens the bound
+                                    const float x = p.alpha_lm * lrow[w];
+                                    const float ub = __fadd_rn(s_ubnl[a2], x);
+                                    if (__fadd_rn(s0, ub) + 1e-5f * (1.0f + fabsf(s0) + ps.z) < thr) continue;
                                 }
-                                if (bt_on) { const float x = p.alpha_bt * cur.btm[2 * k]; ub += x; ua += fabsf(x); }
-                                if (ub_inf) ub = INFINITY;
-                                const float bound = __fadd_rn(s0, ub) + 1e-5f * (1.0f + fabsf(s0) + ua);
-                                if (bound >= thr) {
-                                    int ln, bn;
-                                    const float s = eval(cur, k, s0, w, ln, bn, line >= 0 ? rowval + (size_t)line * VP : nullptr);
-                                    st[line >= 0 ? kEvalDense : kEvalSparse] += 1;
-                                    if (s > kNeg && s >= thr) push_cand(sm, sc, make_key(s, (uint32_t)(k * Vp1 + w)), ln, bn);
+                                int ln, bn;
+                                const float s = eval(cur, k, s0, w, ln, bn, lrow);
+                                st[lrow ? kEvalDense : kEvalSparse] += 1;
+                                if (s > kNeg && s >= thr) {
+                                    const int q = atomicAdd(&sc.nbuf, 1);
+                                    if (q >= cap) { ovf = true; a_from = a2; break; }
+                                    sm.ckey[q] = make_key(s, (uint32_t)(k * Vp1 + w));
+                                    sm.clm[q] = ln; sm.cbt[q] = bn;
                                 }
                             }
+                            if (!ovf) a_from = nalive;
+                            const int any_ovf = __syncthreads_or(ovf);
+                            if (!any_ovf) break;
+                            if (tid == 0) sc.nbuf = cap;  // entries [0, cap) are all written
+                            __syncthreads();
                         }
-                        __syncthreads();
                     }
                 }
             }
@@ -947,7 +973,7 @@ __global__ void order_kernel(const int32_t* __restrict__ lengths, int B, int T, 
 size_t smem_bytes(int K, int Vp1, int R, int cap, int nch, int RWS) {
     const int VP = (Vp1 + 3) & ~3;
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-    size_t s = al(sizeof(float) * (size_t)R * VP);
+    size_t s = al(sizeof(float) * (size_t)R * (VP + 4));
     s += al(8 * K) + al(8 * K) + al(16 * K) + al(8 * K) + al(8 * K) + al(2 * K) + al(8 * (size_t)K * RWS) + al(16 * K);
     s += al(8 * (size_t)cap) + 2 * al(4 * (size_t)cap);
     s += al(8 * K) + 2 * al(4 * K);
@@ -998,7 +1024,11 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
     order_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p.lengths, p.B, p.T, p.order, p.len_c, p.flags, p.B <= 16384);
     e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-    const int nt = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
+    int nt = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
+    if (const char* e_nt = getenv("FLEXCTC_NT")) {  // tuning override (never below the beam)
+        const int want = atoi(e_nt);
+        if ((want == 32 || want == 64 || want == 128 || want == 256) && want >= nt) nt = want;
+    }
     const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
     switch (nt) {
         case 32: return small_lm ? launch_nt<32, 2>(p, st, ev0, ev1, err) : launch_nt<32, kMaxLmLevels>(p, st, ev0, ev1, err);

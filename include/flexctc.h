@@ -155,9 +155,11 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
 void flexctc_set_profile_events(void* ev_start, void* ev_stop);
 
 /* Device counters of the last decode that used `workspace` (call after the stream has
- * synchronised); copies min(n, 16) u64 values: frames, sum of live slots, sum of listed tokens,
+ * synchronised); copies min(n, 32) u64 values: frames, sum of live slots, sum of listed tokens,
  * sparse exact evaluations, dense frames, LM rows built, dense exact evaluations, buffer
- * compactions, top-token stages, deferred next-state queries. */
+ * compactions, top-token stages, deferred next-state queries, then SM cycles (summed over CTAs,
+ * thread 0) of frame phases 1-3, 4, LM row builds, 5, 6-7, the count of frames with listed
+ * tokens and their cycles. */
 flexctc_status flexctc_get_stats(const void* workspace, uint64_t* out, int32_t n);
 
 /* Reads the device flags of the last decode that used `workspace` (call after the stream has

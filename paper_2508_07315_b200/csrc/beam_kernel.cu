@@ -371,7 +371,10 @@ __device__ void build_lm_row(const LmDev& lm, int state, float* row, int V) {
 
 // per-CTA device counters (SURVEY §5 "device counters"), flushed per utterance
 enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEvalDense, kCompactions,
-            kStageA, kDeferredNext, kNumStats };
+            kStageA, kDeferredNext,
+            // SM cycles (thread 0) per frame phase: 1-3, 4, LM row builds (inside 4), 5, 6-7;
+            // frames with listed tokens and their cycles
+            kCycP13, kCycP4, kCycRows, kCycP5, kCycP67, kHeavyFrames, kCycHeavy, kNumStats };
 
 template <int NT, int LMV>
 __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     __shared__ int s_line[kMaxBeam];       // per alive position: row-cache line (-1 = sparse path)
     __shared__ float4 s_pos[kMaxBeam];     // per alive position: {acc, ub, |ub terms|, last}
     __shared__ float s_ubnl[kMaxBeam];     // per alive position: ub without the LM term
+    __shared__ float2 s_suf[kMaxBeam];     // suffix max over positions of {acc, |ub terms|}
     __shared__ int s_build[2 * 32];        // rows to build: (line, state)
     __shared__ int s_nbuild;
     const int tid = threadIdx.x;
@@ -497,6 +501,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             if (tid == 0) { sc.nbuf = 0; sc.m = 0; }
             __syncthreads();
             const float* row = sm.ring + (size_t)(t % R) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
+            const long long c0 = clock64();
 
             // ------------------------------------------------ phase 1: exact blank/repeat candidates,
             // per-slot bounds, frame argmax over non-blank tokens, alive list
@@ -584,8 +589,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             __syncthreads();
 
             // ------------------------------------------------ phase 4: exact non-rb candidates
+            const long long c1 = clock64();
+            const int m_frame = sc.m;
             {
-                const int m = sc.m;
+                const int m = m_frame;
                 if (tid == 0) {
                     st[kFrames] += 1; st[kAlive] += nalive; st[kListed] += m; st[kStageA] += stage_a ? 1 : 0;
                 }
@@ -614,9 +621,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         st[kRowsBuilt] += nb;
                     }
                     __syncthreads();
+                    const long long cr = clock64();
                     for (int i = 0; i < s_nbuild; ++i)
                         build_lm_row<NT>(p.lm, s_build[2 * i + 1], rowval + (size_t)s_build[2 * i] * VP, V);
                     __syncthreads();
+                    if (tid == 0) st[kCycRows] += (uint32_t)(clock64() - cr);
                 } else if (m > 0) {
                     for (int a2 = tid; a2 < nalive; a2 += NT) s_line[a2] = -1;
                 }
@@ -630,6 +639,13 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         if (ub_inf) { ub = INFINITY; ubnl = INFINITY; }
                         s_pos[a2] = make_float4(cur.acc[k], ub, ua, __int_as_float(cur.last[k]));
                         s_ubnl[a2] = ubnl;
+                    }
+                    __syncthreads();
+                    // suffix maxima of acc and |ub terms| over live positions (early exit below)
+                    for (int a2 = tid; a2 < nalive; a2 += NT) {
+                        float am = kNeg, um = 0.0f;
+                        for (int q = a2; q < nalive; ++q) { am = fmaxf(am, s_pos[q].x); um = fmaxf(um, s_pos[q].z); }
+                        s_suf[a2] = make_float2(am, um);
                     }
                     __syncthreads();
                     // token-major: lane = listed token, loop over the live slots. A lane whose push
@@ -653,6 +669,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                             const float thr = sc.thr;
                             bool ovf = false;
                             for (int a2 = a_from; a2 < nalive; ++a2) {
+                                {   // no later live slot can reach thr with this token: stop
+                                    const float2 sf = s_suf[a2];
+                                    const float reach = __fadd_rn(__fadd_rn(sf.x, dw), ubvmax);
+                                    if (reach + 2e-4f * (1.0f + fabsf(sf.x) + fabsf(dw) + fabsf(ubvmax) + sf.y) < thr) break;
+                                }
                                 const float4 ps = s_pos[a2];
                                 if (w == __float_as_int(ps.w)) continue;  // repeat: scored in phase 1
                                 const float s0 = __fadd_rn(ps.x, dw);
@@ -686,6 +707,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             }
 
             // ------------------------------------------------ phase 5: flat TopK + θ-prune
+            const long long c2 = clock64();
             const int n = sc.nbuf;
             const uint64_t* kk;
             const int* kl;
@@ -711,6 +733,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const float mx = nkeep > 0 ? score_of(sm.skey[0]) : kNeg;  // max_score
             const float tau = __fsub_rn(mx, p.theta);
 
+            const long long c3 = clock64();
             // ------------------------------------------------ phase 6: beams.update into nxt
             const int64_t bpo = ((int64_t)b * p.T + t) * K;
             bool live = false, emit = false;
@@ -835,6 +858,12 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             __syncthreads();
             if (tid < K) nxt.acc[tid] = __uint_as_float((uint32_t)sm.skey[tid]);
             cb ^= 1;
+            if (tid == 0) {
+                const long long c4 = clock64();
+                st[kCycP13] += (uint32_t)(c1 - c0); st[kCycP4] += (uint32_t)(c2 - c1);
+                st[kCycP5] += (uint32_t)(c3 - c2); st[kCycP67] += (uint32_t)(c4 - c3);
+                if (m_frame > 0) { st[kHeavyFrames] += 1; st[kCycHeavy] += (uint32_t)(c4 - c0); }
+            }
             __syncthreads();
         }
         cp_wait<0>();

@@ -79,7 +79,7 @@ float lm_query_host(const LmHost& lm, int32_t s, int32_t w, int32_t* next);
 constexpr int kChunk = 32;      // frames per backtrace chunk (chunk ancestors, §7.3 item 6)
 constexpr int kMaxBeam = 256;   // parent index fits a u8
 constexpr int kMaxVp1 = 8192;   // frame rows are staged in shared memory
-constexpr int kStatsWords = 16; // u64 device counters at workspace + 64 B
+constexpr int kStatsWords = 32; // u64 device counters at workspace + 64 B
 
 struct DecodeParams {
     const float* log_probs;

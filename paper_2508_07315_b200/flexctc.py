@@ -54,7 +54,9 @@ EXPORTS = [
     "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_set_profile_events", "flexctc_get_stats",
 ]
 STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
-              "exact_dense", "compactions", "top_token_stages", "deferred_next"]
+              "exact_dense", "compactions", "top_token_stages", "deferred_next",
+              "cyc_phase1_3", "cyc_phase4", "cyc_lm_rows", "cyc_phase5", "cyc_phase6_7", "heavy_frames",
+              "cyc_heavy_frames"]
 
 
 def _load() -> ctypes.CDLL:

@@ -88,12 +88,15 @@ __device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict
     const int n = rec[0], u = rec[1];
     int2 d = make_int2(0, 0);
     if (u >= 0) d = __ldg(&lm.dense[(size_t)u * lm.V + w]);
-    int lo[LMV], hi[LMV], hit[LMV];
+    int lo[LMV], hi[LMV], hlp[LMV], hnx[LMV];
+    bool hit[LMV];
 #pragma unroll
     for (int j = 0; j < LMV; ++j) {
         lo[j] = j < n ? rec[8 + 3 * j] : 0;
         hi[j] = j < n ? lo[j] + rec[8 + 3 * j + 1] : 0;
-        hit[j] = -1;
+        hit[j] = false;
+        hlp[j] = 0;
+        hnx[j] = 0;
     }
     for (;;) {
         bool any = false;
@@ -102,9 +105,9 @@ __device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict
             if (lo[j] < hi[j]) {
                 any = true;
                 const int mid = (lo[j] + hi[j]) >> 1;
-                const int t = __ldg(&lm.arcs[mid]).x;
-                if (t == w) { hit[j] = mid; hi[j] = lo[j]; }
-                else if (t < w) lo[j] = mid + 1;
+                const int4 a = __ldg(&lm.arcs[mid]);  // the whole arc: a hit needs no reload
+                if (a.x == w) { hit[j] = true; hlp[j] = a.y; hnx[j] = a.z; hi[j] = lo[j]; }
+                else if (a.x < w) lo[j] = mid + 1;
                 else hi[j] = mid;
             }
         }
@@ -112,10 +115,9 @@ __device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict
     }
 #pragma unroll
     for (int j = 0; j < LMV; ++j) {
-        if (hit[j] >= 0) {
-            const int4 a = __ldg(&lm.arcs[hit[j]]);
-            next = a.z;
-            return __fadd_rn(__int_as_float(rec[8 + 3 * j + 2]), __int_as_float(a.y));
+        if (hit[j]) {
+            next = hnx[j];
+            return __fadd_rn(__int_as_float(rec[8 + 3 * j + 2]), __int_as_float(hlp[j]));
         }
     }
     if (u >= 0) {
@@ -146,7 +148,7 @@ struct Shared {
 };
 
 struct Scalars {
-    int nbuf, m, nalive, nsel, u;
+    int nbuf, m, nalive, nsel, u, npair;
     float thr;
     uint64_t kth;
     float rf[4][32];
@@ -378,7 +380,7 @@ enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEv
 
 template <int NT, int LMV>
 __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
-                                                      const int nrow) {
+                                                      const int nrow, const int dense_min) {
     constexpr int kRec = (8 + 3 * LMV + 3) & ~3;  // ints per cached LM record
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Scalars sc;
@@ -386,6 +388,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     __shared__ float4 s_pos[kMaxBeam];     // per alive position: {acc, ub, |ub terms|, last}
     __shared__ float s_ubnl[kMaxBeam];     // per alive position: ub without the LM term
     __shared__ float2 s_suf[kMaxBeam];     // suffix max over positions of {acc, |ub terms|}
+    constexpr int kPairCap = 2 * NT;       // viable (position, token) pairs per evaluation batch
+    __shared__ uint32_t s_pairs[kPairCap];
     __shared__ int s_build[2 * 32];        // rows to build: (line, state)
     __shared__ int s_nbuild;
     const int tid = threadIdx.x;
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 cp_commit();
             }
             if (R == 4) cp_wait<3>(); else cp_wait<1>();
-            if (tid == 0) { sc.nbuf = 0; sc.m = 0; }
+            if (tid == 0) { sc.nbuf = 0; sc.m = 0; sc.npair = 0; }
             __syncthreads();
             const float* row = sm.ring + (size_t)(t % R) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
             const long long c0 = clock64();
@@ -598,7 +602,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 }
                 // dense frame: many listed tokens. Score them from LM rows cached in shared memory
                 // (the paper's full-vocabulary NGPU-LM query) instead of per-pair arc searches.
-                const bool dense = lm_on && nrow > 0 && m >= kDenseMinTokens;
+                const bool dense = lm_on && nrow > 0 && m >= dense_min;
                 if (dense) {
                     if (tid == 0) {
                         int nb = 0;
@@ -648,26 +652,19 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         s_suf[a2] = make_float2(am, um);
                     }
                     __syncthreads();
-                    // token-major: lane = listed token, loop over the live slots. A lane whose push
-                    // would overflow the buffer records where it stopped; the block compacts the
-                    // buffer (top K, raised threshold) and the lane resumes there (no duplicates).
+                    // Token-major collection (lane = listed token, loop over the live slots with an
+                    // early exit) of the (position, token) pairs that pass the bounds, then one
+                    // parallel evaluation of the batch (one round of LM arc searches for up to
+                    // kPairCap pairs). A lane whose pair list is full records where it stopped and
+                    // resumes after the batch (no pair is collected twice).
                     for (int base = 0; base < m; base += NT) {
                         const int j = base + tid;
                         const int w = j < m ? (int)sm.toks[j] : -1;
                         const float dw = w >= 0 ? row[w] : 0.0f;
                         int a_from = w >= 0 ? 0 : nalive;
                         for (;;) {
-                            if (sc.nbuf > cap - NT) {
-                                // buffer full: keep the top K, raise the threshold (threshold algorithm)
-                                const int n = sc.nbuf;
-                                const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
-                                gather_selected<NT>(n, kth, sm, sc);
-                                for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
-                                if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); st[kCompactions] += 1; }
-                                __syncthreads();
-                            }
                             const float thr = sc.thr;
-                            bool ovf = false;
+                            bool full = false;
                             for (int a2 = a_from; a2 < nalive; ++a2) {
                                 {   // no later live slot can reach thr with this token: stop
                                     const float2 sf = s_suf[a2];
@@ -678,29 +675,45 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 if (w == __float_as_int(ps.w)) continue;  // repeat: scored in phase 1
                                 const float s0 = __fadd_rn(ps.x, dw);
                                 if (__fadd_rn(s0, ps.y) + 1e-5f * (1.0f + fabsf(s0) + ps.z) < thr) continue;
-                                const int k = sm.alive_idx[a2];
                                 const int line = s_line[a2];
-                                const float* lrow = line >= 0 ? rowval + (size_t)line * VP : nullptr;
-                                if (lrow) {  // exact LM value from the cached row tightens the bound
-                                    const float x = p.alpha_lm * lrow[w];
+                                if (line >= 0) {  // exact LM value from the cached row tightens the bound
+                                    const float x = p.alpha_lm * rowval[(size_t)line * VP + w];
                                     const float ub = __fadd_rn(s_ubnl[a2], x);
                                     if (__fadd_rn(s0, ub) + 1e-5f * (1.0f + fabsf(s0) + ps.z) < thr) continue;
                                 }
-                                int ln, bn;
-                                const float s = eval(cur, k, s0, w, ln, bn, lrow);
-                                st[lrow ? kEvalDense : kEvalSparse] += 1;
-                                if (s > kNeg && s >= thr) {
-                                    const int q = atomicAdd(&sc.nbuf, 1);
-                                    if (q >= cap) { ovf = true; a_from = a2; break; }
-                                    sm.ckey[q] = make_key(s, (uint32_t)(k * Vp1 + w));
-                                    sm.clm[q] = ln; sm.cbt[q] = bn;
-                                }
+                                const int q = atomicAdd(&sc.npair, 1);
+                                if (q >= kPairCap) { full = true; a_from = a2; break; }
+                                s_pairs[q] = ((uint32_t)a2 << 16) | (uint32_t)j;
                             }
-                            if (!ovf) a_from = nalive;
-                            const int any_ovf = __syncthreads_or(ovf);
-                            if (!any_ovf) break;
-                            if (tid == 0) sc.nbuf = cap;  // entries [0, cap) are all written
+                            if (!full) a_from = nalive;
+                            const int any_full = __syncthreads_or(full);
+                            const int np = min(sc.npair, kPairCap);
+                            if (sc.nbuf > cap - np) {
+                                // buffer full: keep the top K, raise the threshold (threshold algorithm)
+                                const int n = sc.nbuf;
+                                const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
+                                gather_selected<NT>(n, kth, sm, sc);
+                                for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
+                                if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); st[kCompactions] += 1; }
+                                __syncthreads();
+                            }
+                            const float thr2 = sc.thr;
+                            for (int q = tid; q < np; q += NT) {
+                                const uint32_t pq = s_pairs[q];
+                                const int a2 = (int)(pq >> 16), jq = (int)(pq & 0xffffu);
+                                const int k = sm.alive_idx[a2];
+                                const int wq = sm.toks[jq];
+                                const int line = s_line[a2];
+                                const float s0 = __fadd_rn(s_pos[a2].x, row[wq]);
+                                int ln, bn;
+                                const float s = eval(cur, k, s0, wq, ln, bn, line >= 0 ? rowval + (size_t)line * VP : nullptr);
+                                st[line >= 0 ? kEvalDense : kEvalSparse] += 1;
+                                if (s > kNeg && s >= thr2) push_cand(sm, sc, make_key(s, (uint32_t)(k * Vp1 + wq)), ln, bn);
+                            }
                             __syncthreads();
+                            if (tid == 0) sc.npair = 0;
+                            __syncthreads();
+                            if (!any_full) break;
                         }
                     }
                 }
@@ -1036,7 +1049,9 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std:
     if (e != cudaSuccess || occ < 1) { err = "occupancy query failed"; return 1; }
     const int grid = std::min(p.B, nsm * occ);
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-    kern<<<grid, NT, sm, st>>>(p, R, cap, nrow);
+    int dense_min = kDenseMinTokens;
+    if (const char* e_dm = getenv("FLEXCTC_DENSE_MIN")) dense_min = std::max(1, atoi(e_dm));  // tuning override
+    kern<<<grid, NT, sm, st>>>(p, R, cap, nrow, dense_min);
     e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }

@@ -376,7 +376,9 @@ enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEv
             kStageA, kDeferredNext,
             // SM cycles (thread 0) per frame phase: 1-3, 4, LM row builds (inside 4), 5, 6-7;
             // frames with listed tokens and their cycles
-            kCycP13, kCycP4, kCycRows, kCycP5, kCycP67, kHeavyFrames, kCycHeavy, kNumStats };
+            kCycP13, kCycP4, kCycRows, kCycP5, kCycP67, kHeavyFrames, kCycHeavy,
+            // finer split: frame top (row issue + wait), phase 2, phase 3, phase 4 setup / collect / evaluate
+            kCycTop, kCycP2, kCycP3, kCycP4Setup, kCycP4Collect, kCycP4Eval, kNumStats };
 
 template <int NT, int LMV>
 __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
@@ -496,6 +498,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         for (int t = 0; t < L; ++t) {
             const Bank cur = bank(cb);
             const Bank nxt = bank(cb ^ 1);
+            const long long ctop = clock64();
             {
                 const int r = t + R - 1;
                 if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1);
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             __syncthreads();
             const float* row = sm.ring + (size_t)(t % R) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
             const long long c0 = clock64();
+            if (tid == 0) st[kCycTop] += (uint32_t)(c0 - ctop);
 
             // ------------------------------------------------ phase 1: exact blank/repeat candidates,
             // per-slot bounds, frame argmax over non-blank tokens, alive list
@@ -546,6 +550,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
 
             // ------------------------------------------------ phase 2: exact candidates of the frame's
             // best non-blank token (tightens the lower bound of the frame max on emission frames)
+            const long long cp2 = clock64();
             bool stage_a = false;
             float tau0 = __fsub_rn(mxrb, p.theta);
             if (nalive > 0 && mxrb > kNeg) {
@@ -571,6 +576,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
 
             // ------------------------------------------------ phase 3: frame token filter
             // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
+            const long long cp3 = clock64();
+            if (tid == 0) st[kCycP2] += (uint32_t)(cp3 - cp2);
             if (nalive > 0 && mxrb > kNeg) {
                 const float mg = 1e-4f * (1.0f + fabsf(tau0) + fabsf(accmax) + fabsf(ubvmax));
                 const float dthr = __fsub_rn(__fsub_rn(__fsub_rn(tau0, accmax), ubvmax), mg);
@@ -589,7 +596,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     }
                 }
             }
-            if (tid == 0) sc.thr = tau0;
+            if (tid == 0) { sc.thr = tau0; st[kCycP3] += (uint32_t)(clock64() - cp3); }
             __syncthreads();
 
             // ------------------------------------------------ phase 4: exact non-rb candidates
@@ -634,6 +641,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     for (int a2 = tid; a2 < nalive; a2 += NT) s_line[a2] = -1;
                 }
                 if (m > 0) {
+                    const long long c4s = clock64();
                     // per live position: {acc, ub (β + α_LM·max P + α_BT·max Δ), |terms|, last}
                     for (int a2 = tid; a2 < nalive; a2 += NT) {
                         const int k = sm.alive_idx[a2];
@@ -652,6 +660,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         s_suf[a2] = make_float2(am, um);
                     }
                     __syncthreads();
+                    long long c4c = clock64();
+                    if (tid == 0) st[kCycP4Setup] += (uint32_t)(c4c - c4s);
                     // Token-major collection (lane = listed token, loop over the live slots with an
                     // early exit) of the (position, token) pairs that pass the bounds, then one
                     // parallel evaluation of the batch (one round of LM arc searches for up to
@@ -687,6 +697,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                             }
                             if (!full) a_from = nalive;
                             const int any_full = __syncthreads_or(full);
+                            const long long c4e = clock64();
+                            if (tid == 0) st[kCycP4Collect] += (uint32_t)(c4e - c4c);
                             const int np = min(sc.npair, kPairCap);
                             if (sc.nbuf > cap - np) {
                                 // buffer full: keep the top K, raise the threshold (threshold algorithm)
@@ -711,7 +723,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 if (s > kNeg && s >= thr2) push_cand(sm, sc, make_key(s, (uint32_t)(k * Vp1 + wq)), ln, bn);
                             }
                             __syncthreads();
-                            if (tid == 0) sc.npair = 0;
+                            c4c = clock64();
+                            if (tid == 0) { sc.npair = 0; st[kCycP4Eval] += (uint32_t)(c4c - c4e); }
                             __syncthreads();
                             if (!any_full) break;
                         }

@@ -56,7 +56,8 @@ EXPORTS = [
 STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
               "exact_dense", "compactions", "top_token_stages", "deferred_next",
               "cyc_phase1_3", "cyc_phase4", "cyc_lm_rows", "cyc_phase5", "cyc_phase6_7", "heavy_frames",
-              "cyc_heavy_frames"]
+              "cyc_heavy_frames", "cyc_frame_top", "cyc_phase2", "cyc_phase3", "cyc_p4_setup", "cyc_p4_collect",
+              "cyc_p4_eval"]
 
 
 def _load() -> ctypes.CDLL:

@@ -65,6 +65,8 @@ __device__ __forceinline__ uint64_t make_key(float s, uint32_t f) {
     return ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - f);
 }
 __device__ __forceinline__ uint32_t flat_of(uint64_t key) { return 0xffffffffu - (uint32_t)key; }
+// (slot k, token w) -> an index ordered exactly like the flat index k·V' + w (w < 2^16)
+__device__ __forceinline__ uint32_t flat_idx(int k, int w) { return ((uint32_t)k << 16) | (uint32_t)w; }
 __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
 __device__ __forceinline__ void cp_async4(void* s, const void* g) {
@@ -569,10 +571,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 tau0 = __fsub_rn(fmaxf(mxrb, mxA), p.theta);  // lower bound of fl(max - θ)
             }
             if (al) {
-                if (sbk > kNeg && sbk >= tau0) push_cand(sm, sc, make_key(sbk, (uint32_t)(tid * Vp1 + blank)), cur.lms[tid], cur.bts[tid]);
-                if (srk > kNeg && srk >= tau0) push_cand(sm, sc, make_key(srk, (uint32_t)(tid * Vp1 + lk)), cur.lms[tid], cur.bts[tid]);
+                if (sbk > kNeg && sbk >= tau0) push_cand(sm, sc, make_key(sbk, flat_idx(tid, blank)), cur.lms[tid], cur.bts[tid]);
+                if (srk > kNeg && srk >= tau0) push_cand(sm, sc, make_key(srk, flat_idx(tid, lk)), cur.lms[tid], cur.bts[tid]);
             }
-            if (sA > kNeg && sA >= tau0) push_cand(sm, sc, make_key(sA, (uint32_t)(kA * Vp1 + wstar)), lnA, bnA);
+            if (sA > kNeg && sA >= tau0) push_cand(sm, sc, make_key(sA, flat_idx(kA, wstar)), lnA, bnA);
 
             // ------------------------------------------------ phase 3: frame token filter
             // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
@@ -720,7 +722,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 int ln, bn;
                                 const float s = eval(cur, k, s0, wq, ln, bn, line >= 0 ? rowval + (size_t)line * VP : nullptr);
                                 st[line >= 0 ? kEvalDense : kEvalSparse] += 1;
-                                if (s > kNeg && s >= thr2) push_cand(sm, sc, make_key(s, (uint32_t)(k * Vp1 + wq)), ln, bn);
+                                if (s > kNeg && s >= thr2) push_cand(sm, sc, make_key(s, flat_idx(k, wq)), ln, bn);
                             }
                             __syncthreads();
                             c4c = clock64();
@@ -774,8 +776,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     if (s >= tau) {
                         live = true;
                         const uint32_t f = flat_of(key);
-                        par = (int)(f / (uint32_t)Vp1);
-                        const int w = (int)(f % (uint32_t)Vp1);
+                        par = (int)(f >> 16);
+                        const int w = (int)(f & 0xffffu);
                         emit = w != blank && w != cur.last[par];
                         int ln = sm.slm[i];
                         const int bn = sm.sbt[i];

@@ -394,6 +394,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     __shared__ float2 s_suf[kMaxBeam];     // suffix max over positions of {acc, |ub terms|}
     constexpr int kPairCap = 2 * NT;       // viable (position, token) pairs per evaluation batch
     __shared__ uint32_t s_pairs[kPairCap];
+    constexpr int kTab = NT > 32 ? 2 * NT : 1;  // recombination table (NT > 32)
+    constexpr int kTabMem = 3;
+    __shared__ unsigned long long s_tkey[kTab];
+    __shared__ int s_tcnt[kTab];
+    __shared__ int s_tmem[kTab * kTabMem];
     __shared__ int s_build[2 * 32];        // rows to build: (line, state)
     __shared__ int s_nbuild;
     const int tid = threadIdx.x;
@@ -822,6 +827,26 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 const unsigned livemask = __ballot_sync(0xffffffffu, lv);
                 grp = __match_any_sync(0xffffffffu, hk) & __match_any_sync(0xffffffffu, lkey) & livemask;
             }
+            int tent = -1;  // NT > 32: this slot's entry in the (hash, last) table
+            if constexpr (NT > 32) {
+                // groups have <= 3 members (reading R14): a shared hash table keyed on (hash, last)
+                // with member lists replaces the O(K) scan per slot
+                for (int e = tid; e < kTab; e += NT) { s_tkey[e] = 0ull; s_tcnt[e] = 0; }
+                __syncthreads();
+                if (tid < K && nxt.acc[tid] > kNeg) {
+                    const uint64_t k2 = (nxt.hash[tid] ^ ((uint64_t)(nxt.last[tid] + 1) * 0x9E3779B97F4A7C15ull)) | 1ull;
+                    int e = (int)((k2 >> 20) & (uint64_t)(kTab - 1));
+                    for (;;) {
+                        const unsigned long long old = atomicCAS(&s_tkey[e], 0ull, (unsigned long long)k2);
+                        if (old == 0ull || old == k2) break;
+                        e = (e + 1) & (kTab - 1);
+                    }
+                    const int q = atomicAdd(&s_tcnt[e], 1);
+                    if (q < kTabMem) s_tmem[e * kTabMem + q] = tid;
+                    tent = e;
+                }
+                __syncthreads();
+            }
             if (tid < K) {
                 const int i = tid;
                 float s = nxt.acc[i];
@@ -840,7 +865,28 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                             s = __fadd_rn(s, (float)log1p((double)sum));
                         }
                     }
-                } else if (s > kNeg) {
+                } else if (s > kNeg && s_tcnt[tent] <= kTabMem) {
+                    const int cnt = s_tcnt[tent];
+                    if (cnt > 1) {
+                        int mem[kTabMem];
+#pragma unroll
+                        for (int q = 0; q < kTabMem; ++q) mem[q] = q < cnt ? s_tmem[tent * kTabMem + q] : 0x7fffffff;
+#pragma unroll
+                        for (int q = 1; q < kTabMem; ++q)  // ascending slot order
+#pragma unroll
+                            for (int r = q; r > 0; --r)
+                                if (mem[r] < mem[r - 1]) { const int x = mem[r]; mem[r] = mem[r - 1]; mem[r - 1] = x; }
+                        if (mem[0] != i) {
+                            s = kNeg;
+                        } else if (p.merge_mode == 0) {
+                            float sum = 0.0f;
+#pragma unroll
+                            for (int q = 1; q < kTabMem; ++q)
+                                if (q < cnt) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(nxt.acc[mem[q]], s)));
+                            s = __fadd_rn(s, (float)log1p((double)sum));
+                        }
+                    }
+                } else if (s > kNeg) {  // oversized group (not expected): plain scan
                     const uint64_t h = nxt.hash[i];
                     const int l = nxt.last[i];
                     bool dead = false;
@@ -1048,13 +1094,15 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std:
     if (sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
     // LM row cache: as many lines as fit a ~110 KB CTA (2 CTAs / SM), at most min(K, 32)
     int nrow = 0;
+    auto kern = ctc_beam_kernel<NT, LMV>;
+    cudaFuncAttributes fattr{};
+    cudaFuncGetAttributes(&fattr, kern);
     if (p.use_lm) {
         const size_t line = 4 * (size_t)VP + 4;
-        const size_t budget = 110 * 1024;
+        const size_t budget = 110 * 1024 - std::min<size_t>(fattr.sharedSizeBytes, 60 * 1024);
         if (sm + 16 < budget) nrow = (int)std::min<size_t>((budget - sm - 16) / line, (size_t)std::min(p.K, 32));
         sm += nrow ? 4 * (size_t)nrow * VP + ((4 * (size_t)nrow + 15) & ~size_t(15)) : 0;
     }
-    auto kern = ctc_beam_kernel<NT, LMV>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     int dev = 0, nsm = 0, occ = 0;

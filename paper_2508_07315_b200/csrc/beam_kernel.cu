@@ -1088,18 +1088,21 @@ template <int NT, int LMV>
 int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
     const int VP = (p.Vp1 + 3) & ~3;
     const int R = VP <= 2048 ? 4 : 2;
-    const int cap = 8 * NT;
+    const int cap = 4 * NT;  // >= 3K phase-1/2 pushes, and >= kPairCap + K for phase 4
     const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
     size_t sm = smem_bytes(p.K, p.Vp1, R, cap, p.nch, RWS) + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) + 16 : 0);
     if (sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
-    // LM row cache: as many lines as fit a ~110 KB CTA (2 CTAs / SM), at most min(K, 32)
+    // LM row cache: as many lines as fit the shared memory left at the register-limited
+    // occupancy (CTAs / SM), at most min(K, 32)
     int nrow = 0;
     auto kern = ctc_beam_kernel<NT, LMV>;
     cudaFuncAttributes fattr{};
     cudaFuncGetAttributes(&fattr, kern);
     if (p.use_lm) {
         const size_t line = 4 * (size_t)VP + 4;
-        const size_t budget = 110 * 1024 - std::min<size_t>(fattr.sharedSizeBytes, 60 * 1024);
+        const int occ_regs = std::max(1, 65536 / std::max(1, fattr.numRegs * NT));
+        const size_t per_cta = std::min<size_t>(200 * 1024, (size_t)(224 * 1024) / (size_t)occ_regs);
+        const size_t budget = per_cta - std::min<size_t>(fattr.sharedSizeBytes, per_cta / 2);
         if (sm + 16 < budget) nrow = (int)std::min<size_t>((budget - sm - 16) / line, (size_t)std::min(p.K, 32));
         sm += nrow ? 4 * (size_t)nrow * VP + ((4 * (size_t)nrow + 15) & ~size_t(15)) : 0;
     }
@@ -1131,10 +1134,13 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
     order_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p.lengths, p.B, p.T, p.order, p.len_c, p.flags, p.B <= 16384);
     e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-    int nt = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
+    // 8 warps per utterance: the frame scans, the pair collection/evaluation and the selection
+    // parallelise over tokens, which shortens the latency-bound frame step (measured on c2-c5)
+    int nt = 256;
     if (const char* e_nt = getenv("FLEXCTC_NT")) {  // tuning override (never below the beam)
         const int want = atoi(e_nt);
-        if ((want == 32 || want == 64 || want == 128 || want == 256) && want >= nt) nt = want;
+        const int need = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
+        if ((want == 32 || want == 64 || want == 128 || want == 256) && want >= need) nt = want;
     }
     const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
     switch (nt) {

@@ -45,7 +45,7 @@ namespace flexctc {
 namespace {
 
 constexpr float kNeg = -INFINITY;
-constexpr int kDenseMinTokens = 24;                 // listed tokens per frame that switch to LM rows
+constexpr int kDenseMinTokens = 24;  // listed tokens per frame that switch to LM rows (when enabled)
 
 __device__ __forceinline__ uint64_t hash_extend(uint64_t h, int w) {  // SPEC S:58 (FNV-64 prime)
     return (h ^ (uint64_t)(w + 1)) * 1099511628211ull;
@@ -819,7 +819,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             __syncthreads();
             // ------------------------------------------------ phase 7: RecombineHypotheses
             unsigned grp = 0;
-            if constexpr (NT == 32) {
+            const bool small_beam = K <= 32;  // all slots live in warp 0
+            if (small_beam && tid < 32) {
                 // one warp holds the beam: group lanes by (hash, last) with match.any
                 const bool lv = tid < K && nxt.acc[tid] > kNeg;
                 const uint64_t hk = lv ? nxt.hash[tid] : (0xfedcba9800000000ull | (uint64_t)tid);
@@ -827,8 +828,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 const unsigned livemask = __ballot_sync(0xffffffffu, lv);
                 grp = __match_any_sync(0xffffffffu, hk) & __match_any_sync(0xffffffffu, lkey) & livemask;
             }
-            int tent = -1;  // NT > 32: this slot's entry in the (hash, last) table
-            if constexpr (NT > 32) {
+            int tent = -1;  // K > 32: this slot's entry in the (hash, last) table
+            if (NT > 32 && !small_beam) {
                 // groups have <= 3 members (reading R14): a shared hash table keyed on (hash, last)
                 // with member lists replaces the O(K) scan per slot
                 for (int e = tid; e < kTab; e += NT) { s_tkey[e] = 0ull; s_tcnt[e] = 0; }
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             if (tid < K) {
                 const int i = tid;
                 float s = nxt.acc[i];
-                if (NT == 32 && s > kNeg) {
+                if (small_beam && s > kNeg) {
                     if (grp & ((1u << i) - 1u)) {
                         s = kNeg;  // a better (lower) slot of the group survives
                     } else {
@@ -1098,7 +1099,12 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std:
     auto kern = ctc_beam_kernel<NT, LMV>;
     cudaFuncAttributes fattr{};
     cudaFuncGetAttributes(&fattr, kern);
-    if (p.use_lm) {
+    // The dense-frame LM row cache is off by default: with 8 warps per utterance the batched
+    // sparse evaluation is faster on c3-c5 (measured); FLEXCTC_DENSE_MIN=<tokens> enables it.
+    int dense_min = kDenseMinTokens;
+    const char* e_dm = getenv("FLEXCTC_DENSE_MIN");
+    if (e_dm) dense_min = std::max(1, atoi(e_dm));
+    if (p.use_lm && e_dm) {
         const size_t line = 4 * (size_t)VP + 4;
         const int occ_regs = std::max(1, 65536 / std::max(1, fattr.numRegs * NT));
         const size_t per_cta = std::min<size_t>(200 * 1024, (size_t)(224 * 1024) / (size_t)occ_regs);
@@ -1115,8 +1121,6 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std:
     if (e != cudaSuccess || occ < 1) { err = "occupancy query failed"; return 1; }
     const int grid = std::min(p.B, nsm * occ);
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-    int dense_min = kDenseMinTokens;
-    if (const char* e_dm = getenv("FLEXCTC_DENSE_MIN")) dense_min = std::max(1, atoi(e_dm));  // tuning override
     kern<<<grid, NT, sm, st>>>(p, R, cap, nrow, dense_min);
     e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);

@@ -150,17 +150,22 @@ struct Shared {
 };
 
 struct Scalars {
-    int nbuf, m, nalive, nsel, u, npair;
-    float thr;
+    int nbuf, m, nalive, nsel, u, npair, excl, scan;
+    float thr, ubvmax, dthr;
     uint64_t kth;
     float rf[4][32];
     uint64_t rk[32];
     int ri[32];
 };
 
-template <int NT>
-__device__ __forceinline__ float block_max(float v, Scalars& sc) {
-    constexpr int NW = NT / 32;
+// Group-level primitives. A group is either the whole CTA (G = blockDim) or warp 0 alone
+// (G = 32, the beam warp of the K <= 32 kernel mode); gsync is the matching barrier.
+__device__ __forceinline__ void gsync(int G) {
+    if (G == 32) __syncwarp(); else __syncthreads();
+}
+
+__device__ __forceinline__ float block_max(float v, Scalars& sc, int G) {
+    const int NW = G >> 5;
 #pragma unroll
     for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (NW == 1) return v;
@@ -169,14 +174,12 @@ __device__ __forceinline__ float block_max(float v, Scalars& sc) {
     if (lane == 0) sc.rf[0][wid] = v;
     __syncthreads();
     float r = sc.rf[0][0];
-#pragma unroll
     for (int i = 1; i < NW; ++i) r = fmaxf(r, sc.rf[0][i]);
     return r;
 }
 
-template <int NT>
-__device__ __forceinline__ uint64_t block_max_u64(uint64_t v, Scalars& sc) {
-    constexpr int NW = NT / 32;
+__device__ __forceinline__ uint64_t block_max_u64(uint64_t v, Scalars& sc, int G) {
+    const int NW = G >> 5;
 #pragma unroll
     for (int o = 16; o; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (NW == 1) return v;
@@ -185,17 +188,15 @@ __device__ __forceinline__ uint64_t block_max_u64(uint64_t v, Scalars& sc) {
     if (lane == 0) sc.rk[wid] = v;
     __syncthreads();
     uint64_t r = sc.rk[0];
-#pragma unroll
     for (int i = 1; i < NW; ++i) r = umax64(r, sc.rk[i]);
     return r;
 }
 
 // Phase-1 reduction in one round: max of three floats, max of a u64 key, exclusive scan of a
 // 0/1 flag (slot order). Returns via references.
-template <int NT>
 __device__ __forceinline__ void block_reduce_p1(float& a, float& b, float& c, uint64_t& k, bool flag, int& off,
-                                                int& tot, Scalars& sc) {
-    constexpr int NW = NT / 32;
+                                                int& tot, Scalars& sc, int G) {
+    const int NW = G >> 5;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -219,7 +220,6 @@ __device__ __forceinline__ void block_reduce_p1(float& a, float& b, float& c, ui
     __syncthreads();
     a = sc.rf[0][0]; b = sc.rf[1][0]; c = sc.rf[2][0]; k = sc.rk[0];
     int base = 0, all = 0;
-#pragma unroll
     for (int i = 0; i < NW; ++i) {
         if (i) { a = fmaxf(a, sc.rf[0][i]); b = fmaxf(b, sc.rf[1][i]); c = fmaxf(c, sc.rf[2][i]); k = umax64(k, sc.rk[i]); }
         if (i < wid) base += sc.ri[i];
@@ -229,10 +229,9 @@ __device__ __forceinline__ void block_reduce_p1(float& a, float& b, float& c, ui
     tot = all;
 }
 
-// exclusive prefix over the block of per-thread counts; returns the offset, total in *tot
-template <int NT>
-__device__ __forceinline__ int block_exscan(int v, int* tot, Scalars& sc) {
-    constexpr int NW = NT / 32;
+// exclusive prefix over the group of per-thread counts; returns the offset, total in *tot
+__device__ __forceinline__ int block_exscan(int v, int* tot, Scalars& sc, int G) {
+    const int NW = G >> 5;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int x = v;
 #pragma unroll
@@ -240,11 +239,14 @@ __device__ __forceinline__ int block_exscan(int v, int* tot, Scalars& sc) {
         const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
+    if (NW == 1) {
+        *tot = __shfl_sync(0xffffffffu, x, 31);
+        return x - v;
+    }
     __syncthreads();
     if (lane == 31) sc.ri[wid] = x;
     __syncthreads();
     int base = 0, all = 0;
-#pragma unroll
     for (int i = 0; i < NW; ++i) {
         if (i < wid) base += sc.ri[i];
         all += sc.ri[i];
@@ -255,18 +257,17 @@ __device__ __forceinline__ int block_exscan(int v, int* tot, Scalars& sc) {
 
 // Radix select over n unique 64-bit keys in smem: returns kth such that exactly K keys are
 // >= kth (requires n > K). MSB-first 8-bit digits; stops as soon as the boundary bin is exact.
-template <int NT>
-__device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Scalars& sc) {
+__device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Scalars& sc, int G) {
     uint64_t prefix = 0, mask = 0;
     int remaining = K;
     for (int shift = 56; shift >= 0; shift -= 8) {
-        for (int i = threadIdx.x; i < 256; i += NT) sm.hist[i] = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += NT) {
+        for (int i = threadIdx.x; i < 256; i += G) sm.hist[i] = 0;
+        gsync(G);
+        for (int i = threadIdx.x; i < n; i += G) {
             const uint64_t k = keys[i];
             if ((k & mask) == prefix) atomicAdd(&sm.hist[(k >> shift) & 255u], 1u);
         }
-        __syncthreads();
+        gsync(G);
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;  // lane l owns digits 255-8l .. 248-8l (descending)
             uint32_t c[8];
@@ -293,10 +294,10 @@ __device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Sc
                 }
             }
         }
-        __syncthreads();
+        gsync(G);
         const uint64_t d = sc.kth;
         const int need = sc.ri[0], inbin = sc.ri[1];
-        __syncthreads();
+        gsync(G);
         prefix |= d << shift;
         mask |= 255ull << shift;
         remaining = need;
@@ -306,18 +307,17 @@ __device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Sc
 }
 
 // Move the keys >= kth (exactly K of them) from the candidate buffer into the selection arrays.
-template <int NT>
-__device__ void gather_selected(int n, uint64_t kth, Shared& sm, Scalars& sc) {
+__device__ void gather_selected(int n, uint64_t kth, Shared& sm, Scalars& sc, int G) {
     if (threadIdx.x == 0) sc.nsel = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += NT) {
+    gsync(G);
+    for (int i = threadIdx.x; i < n; i += G) {
         const uint64_t k = sm.ckey[i];
         if (k >= kth) {
             const int j = atomicAdd(&sc.nsel, 1);
             sm.skey[j] = k; sm.slm[j] = sm.clm[i]; sm.sbt[j] = sm.cbt[i];
         }
     }
-    __syncthreads();
+    gsync(G);
 }
 
 __device__ __forceinline__ void push_cand(Shared& sm, Scalars& sc, uint64_t key, int lmn, int btn) {
@@ -330,18 +330,20 @@ __device__ __forceinline__ void push_cand(Shared& sm, Scalars& sc, uint64_t key,
 // 16-B cp.async except for <= 3 head and tail elements.
 __device__ __forceinline__ int row_off(const float* src) { return (int)(((uintptr_t)src >> 2) & 3); }
 
-template <int NT>
-__device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1) {
-    const int tid = threadIdx.x;
+// issued by `nt` threads with local index `tid` (all threads, or the helper warps)
+__device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1, int tid, int nt) {
     const int off = row_off(src);
     float* dst = slot + off;
     const int h = min((4 - off) & 3, Vp1);
     if (tid < h) cp_async4(dst + tid, src + tid);
     const int n4 = (Vp1 - h) >> 2;
-    for (int i = tid; i < n4; i += NT) cp_async16(dst + h + 4 * i, src + h + 4 * i);
+    for (int i = tid; i < n4; i += nt) cp_async16(dst + h + 4 * i, src + h + 4 * i);
     const int t0 = h + 4 * n4;
     if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
 }
+
+// barrier among the helper warps only (named barrier 2)
+__device__ __forceinline__ void helpers_sync(int n) { asm volatile("bar.sync 2, %0;" ::"r"(n) : "memory"); }
 
 // Fill an LM row: row[w] = log P(w | state) for every decoder token w, in exactly the fp32
 // arithmetic of lm_query (dense level-1 path first, then arc levels from the shortest context to
@@ -401,6 +403,19 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     __shared__ int s_tmem[kTab * kTabMem];
     __shared__ int s_build[2 * 32];        // rows to build: (line, state)
     __shared__ int s_nbuild;
+    // solo mode (K <= 32, NT > 32): warp 0 runs the slot-serial phases with warp-level sync;
+    // warps 1.. ("helpers") stream the rows and precompute each frame's summary one frame ahead
+    // (best non-blank token + every token within kListDelta of it, up to kListCap), and join the
+    // beam warp only for frames whose candidate list the summary cannot provide.
+    constexpr int kListCap = 32;
+    constexpr float kListDelta = 16.0f;
+    constexpr int kRing = 4;
+    __shared__ unsigned long long s_sum_key[kRing];
+    __shared__ float s_sum_floor[kRing];
+    __shared__ int s_sum_cnt[kRing];
+    __shared__ int s_list_tok[kRing * kListCap];
+    __shared__ float s_list_d[kRing * kListCap];
+    __shared__ unsigned long long s_hkey[32];
     const int tid = threadIdx.x;
     const int K = p.K, Vp1 = p.Vp1, blank = Vp1 - 1, V = Vp1 - 1;
     const int VP = (Vp1 + 3) & ~3;
@@ -408,6 +423,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
     const int RWS = lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
+    const bool solo = K <= 32 && NT > 32 && R == kRing && !p.solo_off;
+    const bool helper = solo && tid >= 32;
+    const bool bw = !solo || tid < 32;               // takes part in the slot-serial phases
+    const int ltid = helper ? tid - 32 : tid;        // row loader index / count
+    const int lnt = solo ? NT - 32 : NT;
     uint32_t st[kNumStats] = {};
 
     Shared sm;
@@ -496,127 +516,203 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 c0.btm[1] = bt_on ? __ldg(&p.bt.U[0]) : 0.0f;
             }
         }
-        for (int r = 0; r < R - 1; ++r) {  // prologue: rows 0..R-2
-            if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1);
-            cp_commit();
-        }
+        // Row prefetch: in solo mode the helper warps own the ring (distance 2, so the beam warp
+        // can still read row t while helpers fill row t+2); otherwise all threads (distance R-1).
+        const int pf = solo ? 2 : R - 1;
+        if (!solo || helper)
+            for (int r = 0; r < pf; ++r) {  // prologue
+                if (r < L) load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt);
+                cp_commit();
+            }
 
-        int cb = 0;  // current bank
         for (int t = 0; t < L; ++t) {
+            const int cb = t & 1;  // current bank (every thread tracks it, helpers included)
             const Bank cur = bank(cb);
             const Bank nxt = bank(cb ^ 1);
             const long long ctop = clock64();
-            {
-                const int r = t + R - 1;
-                if (r < L) load_row<NT>(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1);
+            const int slot = t % R;
+            float* ring_t = sm.ring + (size_t)slot * (VP + 4);
+            const float* row = ring_t + row_off(Db + (int64_t)t * p.stride_t);
+            if (!solo || helper) {
+                const int r = t + pf;
+                if (r < L) load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt);
                 cp_commit();
+                if (solo) cp_wait<2>(); else if (R == 4) cp_wait<3>(); else cp_wait<1>();
             }
-            if (R == 4) cp_wait<3>(); else cp_wait<1>();
-            if (tid == 0) { sc.nbuf = 0; sc.m = 0; sc.npair = 0; }
-            __syncthreads();
-            const float* row = sm.ring + (size_t)(t % R) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
-            const long long c0 = clock64();
-            if (tid == 0) st[kCycTop] += (uint32_t)(c0 - ctop);
-
-            // ------------------------------------------------ phase 1: exact blank/repeat candidates,
-            // per-slot bounds, frame argmax over non-blank tokens, alive list
-            float a = kNeg, sbk = kNeg, srk = kNeg, ubk = kNeg, uak = 0.0f;
-            int lk = blank;
-            bool al = false;
-            if (tid < K) {
-                a = cur.acc[tid];
-                al = a > kNeg;
-                lk = cur.last[tid];
-                if (al) {
-                    sbk = __fadd_rn(a, row[blank]);                 // blank: no β / fusion
-                    if (lk != blank) srk = __fadd_rn(a, row[lk]);    // repeat: no β / fusion
-                    float ub = p.beta, ua = fabsf(p.beta);
-                    if (lm_on) { const float x = p.alpha_lm * __int_as_float(cur.rec[tid * RWS + 4]); ub += x; ua += fabsf(x); }
-                    if (bt_on) { const float x = p.alpha_bt * cur.btm[2 * tid]; ub += x; ua += fabsf(x); }
-                    ubk = ub_inf ? INFINITY : ub;
-                    uak = ua;
-                }
-            }
-            uint64_t best_tok = 0;
-            {
+            if (helper) {
+                // frame summary for the beam warp: best non-blank token and the complete list of
+                // tokens within kListDelta of it (capped at 32; the count says when it overflowed)
+                const int h = ltid;
+                if (h == 0) s_sum_cnt[slot] = 0;
                 float bv = kNeg;
                 int bi = -1;
-                for (int w = tid; w < blank; w += NT) {  // blank is the last index (R1)
+                for (int w = h; w < blank; w += lnt) {
                     const float v = row[w];
                     if (v > bv || bi < 0) { bv = v; bi = w; }
                 }
-                if (bi >= 0) best_tok = make_key(bv, (uint32_t)bi);
-            }
-            float mxrb = fmaxf(sbk, srk), accmax = a, ubvmax = ubk;
-            int aoff, nalive;
-            block_reduce_p1<NT>(mxrb, accmax, ubvmax, best_tok, al, aoff, nalive, sc);
-            if (al) sm.alive_idx[aoff] = tid;
-            const int wstar = (int)flat_of(best_tok);
-            const float dstar = score_of(best_tok);
-            __syncthreads();
-
-            // ------------------------------------------------ phase 2: exact candidates of the frame's
-            // best non-blank token (tightens the lower bound of the frame max on emission frames)
-            const long long cp2 = clock64();
-            bool stage_a = false;
-            float tau0 = __fsub_rn(mxrb, p.theta);
-            if (nalive > 0 && mxrb > kNeg) {
-                const float reach = __fadd_rn(__fadd_rn(accmax, dstar), ubvmax) +
-                                    1e-4f * (1.0f + fabsf(accmax) + fabsf(dstar) + fabsf(ubvmax));
-                stage_a = reach >= mxrb;
-            }
-            float sA = kNeg;
-            int lnA = 0, bnA = 0, kA = -1;
-            if (stage_a) {
-                if (tid < nalive) {
-                    kA = sm.alive_idx[tid];
-                    if (wstar != cur.last[kA]) sA = eval(cur, kA, __fadd_rn(cur.acc[kA], dstar), wstar, lnA, bnA, nullptr);
-                }
-                const float mxA = block_max<NT>(sA, sc);
-                tau0 = __fsub_rn(fmaxf(mxrb, mxA), p.theta);  // lower bound of fl(max - θ)
-            }
-            if (al) {
-                if (sbk > kNeg && sbk >= tau0) push_cand(sm, sc, make_key(sbk, flat_idx(tid, blank)), cur.lms[tid], cur.bts[tid]);
-                if (srk > kNeg && srk >= tau0) push_cand(sm, sc, make_key(srk, flat_idx(tid, lk)), cur.lms[tid], cur.bts[tid]);
-            }
-            if (sA > kNeg && sA >= tau0) push_cand(sm, sc, make_key(sA, flat_idx(kA, wstar)), lnA, bnA);
-
-            // ------------------------------------------------ phase 3: frame token filter
-            // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
-            const long long cp3 = clock64();
-            if (tid == 0) st[kCycP2] += (uint32_t)(cp3 - cp2);
-            if (nalive > 0 && mxrb > kNeg) {
-                const float mg = 1e-4f * (1.0f + fabsf(tau0) + fabsf(accmax) + fabsf(ubvmax));
-                const float dthr = __fsub_rn(__fsub_rn(__fsub_rn(tau0, accmax), ubvmax), mg);
-                const bool maybe = stage_a ? true : (dstar >= dthr);
-                if (maybe) {
-                    for (int w0 = 0; w0 < Vp1; w0 += NT) {
-                        const int w = w0 + tid;
-                        const bool hit = w < Vp1 && w != blank && !(stage_a && w == wstar) && row[w] >= dthr;
-                        const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                        if (bal) {
-                            int base = 0;
-                            if ((tid & 31) == 0) base = atomicAdd(&sc.m, __popc(bal));
-                            base = __shfl_sync(0xffffffffu, base, 0);
-                            if (hit) sm.toks[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = (uint16_t)w;
-                        }
+                uint64_t key = bi >= 0 ? make_key(bv, (uint32_t)bi) : 0ull;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) key = umax64(key, __shfl_xor_sync(0xffffffffu, key, o));
+                if ((tid & 31) == 0) s_hkey[(tid >> 5) - 1] = key;
+                helpers_sync(lnt);
+                uint64_t best = s_hkey[0];
+                for (int i = 1; i < (lnt >> 5); ++i) best = umax64(best, s_hkey[i]);
+                const float dmax = score_of(best);
+                const float floor_ = __fsub_rn(dmax, kListDelta);
+                for (int w0 = 0; w0 < blank; w0 += lnt) {
+                    const int w = w0 + h;
+                    const bool hit = w < blank && row[w] >= floor_;
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (bal) {
+                        int base = 0;
+                        if ((tid & 31) == 0) base = atomicAdd(&s_sum_cnt[slot], __popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        const int q = base + __popc(bal & ((1u << (tid & 31)) - 1u));
+                        if (hit && q < kListCap) { s_list_tok[slot * kListCap + q] = w; s_list_d[slot * kListCap + q] = row[w]; }
                     }
                 }
+                if (h == 0) { s_sum_key[slot] = best; s_sum_floor[slot] = floor_; }
             }
-            if (tid == 0) { sc.thr = tau0; st[kCycP3] += (uint32_t)(clock64() - cp3); }
-            __syncthreads();
+            if (tid == 0) { sc.nbuf = 0; sc.m = 0; sc.npair = 0; }
+            __syncthreads();  // B0: row t and its summary are ready
+            const long long c0 = clock64();
+            if (tid == 0) st[kCycTop] += (uint32_t)(c0 - ctop);
+
+            const int G = solo ? 32 : NT;  // group of the slot-parallel phases
+            bool stage_a = false;
+            int wstar = -1;
+            if (bw) {
+                // ------------------------------------------------ phase 1: exact blank/repeat candidates,
+                // per-slot bounds, frame argmax over non-blank tokens, alive list
+                float a = kNeg, sbk = kNeg, srk = kNeg, ubk = kNeg;
+                int lk = blank;
+                bool al = false;
+                if (tid < K) {
+                    a = cur.acc[tid];
+                    al = a > kNeg;
+                    lk = cur.last[tid];
+                    if (al) {
+                        sbk = __fadd_rn(a, row[blank]);                 // blank: no β / fusion
+                        if (lk != blank) srk = __fadd_rn(a, row[lk]);    // repeat: no β / fusion
+                        float ub = p.beta;
+                        if (lm_on) ub += p.alpha_lm * __int_as_float(cur.rec[tid * RWS + 4]);
+                        if (bt_on) ub += p.alpha_bt * cur.btm[2 * tid];
+                        ubk = ub_inf ? INFINITY : ub;
+                    }
+                }
+                uint64_t best_tok = 0;
+                if (solo) {
+                    best_tok = s_sum_key[slot];
+                } else {
+                    float bv = kNeg;
+                    int bi = -1;
+                    for (int w = tid; w < blank; w += NT) {  // blank is the last index (R1)
+                        const float v = row[w];
+                        if (v > bv || bi < 0) { bv = v; bi = w; }
+                    }
+                    if (bi >= 0) best_tok = make_key(bv, (uint32_t)bi);
+                }
+                float mxrb = fmaxf(sbk, srk), accmax = a, ubvmax = ubk;
+                int aoff, nalive;
+                block_reduce_p1(mxrb, accmax, ubvmax, best_tok, al, aoff, nalive, sc, G);
+                if (al) sm.alive_idx[aoff] = tid;
+                wstar = (int)flat_of(best_tok);
+                const float dstar = score_of(best_tok);
+                gsync(G);
+
+                // ------------------------------------------------ phase 2: exact candidates of the frame's
+                // best non-blank token (tightens the lower bound of the frame max on emission frames)
+                const long long cp2 = clock64();
+                float tau0 = __fsub_rn(mxrb, p.theta);
+                if (nalive > 0 && mxrb > kNeg) {
+                    const float reach = __fadd_rn(__fadd_rn(accmax, dstar), ubvmax) +
+                                        1e-4f * (1.0f + fabsf(accmax) + fabsf(dstar) + fabsf(ubvmax));
+                    stage_a = reach >= mxrb;
+                }
+                float sA = kNeg;
+                int lnA = 0, bnA = 0, kA = -1;
+                if (stage_a) {
+                    if (tid < nalive) {
+                        kA = sm.alive_idx[tid];
+                        if (wstar != cur.last[kA]) sA = eval(cur, kA, __fadd_rn(cur.acc[kA], dstar), wstar, lnA, bnA, nullptr);
+                    }
+                    const float mxA = block_max(sA, sc, G);
+                    tau0 = __fsub_rn(fmaxf(mxrb, mxA), p.theta);  // lower bound of fl(max - θ)
+                }
+                if (al) {
+                    if (sbk > kNeg && sbk >= tau0) push_cand(sm, sc, make_key(sbk, flat_idx(tid, blank)), cur.lms[tid], cur.bts[tid]);
+                    if (srk > kNeg && srk >= tau0) push_cand(sm, sc, make_key(srk, flat_idx(tid, lk)), cur.lms[tid], cur.bts[tid]);
+                }
+                if (sA > kNeg && sA >= tau0) push_cand(sm, sc, make_key(sA, flat_idx(kA, wstar)), lnA, bnA);
+
+                // ------------------------------------------------ phase 3 (decision): token filter
+                // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
+                const long long cp3 = clock64();
+                if (tid == 0) st[kCycP2] += (uint32_t)(cp3 - cp2);
+                bool scan = false;
+                float dthr = INFINITY;
+                if (nalive > 0 && mxrb > kNeg) {
+                    const float mg = 1e-4f * (1.0f + fabsf(tau0) + fabsf(accmax) + fabsf(ubvmax));
+                    dthr = __fsub_rn(__fsub_rn(__fsub_rn(tau0, accmax), ubvmax), mg);
+                    scan = stage_a ? true : (dstar >= dthr);
+                }
+                bool heavy = false;
+                if (solo && scan) {
+                    // the summary's list holds every token >= floor: usable when dthr >= floor
+                    const int cnt = s_sum_cnt[slot];
+                    if (cnt <= kListCap && dthr >= s_sum_floor[slot]) {
+                        const int j = tid;
+                        const int w = j < cnt ? s_list_tok[slot * kListCap + j] : -1;
+                        const bool hit = w >= 0 && w != blank && !(stage_a && w == wstar) &&
+                                         s_list_d[slot * kListCap + j] >= dthr;
+                        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                        if (hit) sm.toks[__popc(bal & ((1u << tid) - 1u))] = (uint16_t)w;
+                        if (tid == 0) sc.m = __popc(bal);
+                    } else {
+                        heavy = true;
+                    }
+                }
+                if (tid == 0) {
+                    sc.thr = tau0; sc.nalive = nalive; sc.ubvmax = ubvmax; sc.dthr = dthr;
+                    sc.excl = stage_a ? wstar : -1; sc.scan = (!solo && scan) || heavy;
+                    st[kStageA] += stage_a ? 1 : 0;
+                }
+            }
+            if (solo) __syncthreads();  // B1: the helpers learn whether this frame needs them
+            gsync(G);
+            const bool scan_all = sc.scan;
+            const int nalive = sc.nalive;
+            const float ubvmax = sc.ubvmax;
+            if (scan_all) {  // full filter scan of the row by the whole CTA
+                const float dthr = sc.dthr;
+                const int excl = sc.excl;
+                for (int w0 = 0; w0 < Vp1; w0 += NT) {
+                    const int w = w0 + tid;
+                    const bool hit = w < Vp1 && w != blank && w != excl && row[w] >= dthr;
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (bal) {
+                        int base = 0;
+                        if ((tid & 31) == 0) base = atomicAdd(&sc.m, __popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (hit) sm.toks[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = (uint16_t)w;
+                    }
+                }
+                __syncthreads();
+            }
+            if (tid == 0) st[kCycP3] += (uint32_t)(clock64() - c0);
+            // group of phase 4: the whole CTA when it scanned, else the beam warp alone (solo)
+            const int G4 = (solo && !scan_all) ? 32 : NT;
+            if (solo && helper && !scan_all) continue;  // helpers go on to the next row + summary
 
             // ------------------------------------------------ phase 4: exact non-rb candidates
             const long long c1 = clock64();
             const int m_frame = sc.m;
             {
                 const int m = m_frame;
-                if (tid == 0) {
-                    st[kFrames] += 1; st[kAlive] += nalive; st[kListed] += m; st[kStageA] += stage_a ? 1 : 0;
-                }
+                if (tid == 0) { st[kFrames] += 1; st[kAlive] += nalive; st[kListed] += m; }
                 // dense frame: many listed tokens. Score them from LM rows cached in shared memory
                 // (the paper's full-vocabulary NGPU-LM query) instead of per-pair arc searches.
-                const bool dense = lm_on && nrow > 0 && m >= dense_min;
+                const bool dense = lm_on && nrow > 0 && m >= dense_min && G4 == NT;
                 if (dense) {
                     if (tid == 0) {
                         int nb = 0;
@@ -645,12 +741,12 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     __syncthreads();
                     if (tid == 0) st[kCycRows] += (uint32_t)(clock64() - cr);
                 } else if (m > 0) {
-                    for (int a2 = tid; a2 < nalive; a2 += NT) s_line[a2] = -1;
+                    for (int a2 = tid; a2 < nalive; a2 += G4) s_line[a2] = -1;
                 }
                 if (m > 0) {
                     const long long c4s = clock64();
                     // per live position: {acc, ub (β + α_LM·max P + α_BT·max Δ), |terms|, last}
-                    for (int a2 = tid; a2 < nalive; a2 += NT) {
+                    for (int a2 = tid; a2 < nalive; a2 += G4) {
                         const int k = sm.alive_idx[a2];
                         float ub = p.beta, ua = fabsf(p.beta), ubnl = p.beta;
                         if (lm_on) { const float x = p.alpha_lm * __int_as_float(cur.rec[k * RWS + 4]); ub += x; ua += fabsf(x); }
@@ -659,14 +755,14 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         s_pos[a2] = make_float4(cur.acc[k], ub, ua, __int_as_float(cur.last[k]));
                         s_ubnl[a2] = ubnl;
                     }
-                    __syncthreads();
+                    gsync(G4);
                     // suffix maxima of acc and |ub terms| over live positions (early exit below)
-                    for (int a2 = tid; a2 < nalive; a2 += NT) {
+                    for (int a2 = tid; a2 < nalive; a2 += G4) {
                         float am = kNeg, um = 0.0f;
                         for (int q = a2; q < nalive; ++q) { am = fmaxf(am, s_pos[q].x); um = fmaxf(um, s_pos[q].z); }
                         s_suf[a2] = make_float2(am, um);
                     }
-                    __syncthreads();
+                    gsync(G4);
                     long long c4c = clock64();
                     if (tid == 0) st[kCycP4Setup] += (uint32_t)(c4c - c4s);
                     // Token-major collection (lane = listed token, loop over the live slots with an
@@ -674,7 +770,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     // parallel evaluation of the batch (one round of LM arc searches for up to
                     // kPairCap pairs). A lane whose pair list is full records where it stopped and
                     // resumes after the batch (no pair is collected twice).
-                    for (int base = 0; base < m; base += NT) {
+                    for (int base = 0; base < m; base += G4) {
                         const int j = base + tid;
                         const int w = j < m ? (int)sm.toks[j] : -1;
                         const float dw = w >= 0 ? row[w] : 0.0f;
@@ -703,21 +799,21 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 s_pairs[q] = ((uint32_t)a2 << 16) | (uint32_t)j;
                             }
                             if (!full) a_from = nalive;
-                            const int any_full = __syncthreads_or(full);
+                            const int any_full = G4 == 32 ? (int)__any_sync(0xffffffffu, full) : __syncthreads_or(full);
                             const long long c4e = clock64();
                             if (tid == 0) st[kCycP4Collect] += (uint32_t)(c4e - c4c);
                             const int np = min(sc.npair, kPairCap);
                             if (sc.nbuf > cap - np) {
                                 // buffer full: keep the top K, raise the threshold (threshold algorithm)
                                 const int n = sc.nbuf;
-                                const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
-                                gather_selected<NT>(n, kth, sm, sc);
-                                for (int i = tid; i < K; i += NT) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
+                                const uint64_t kth = radix_kth(sm.ckey, n, K, sm, sc, G4);
+                                gather_selected(n, kth, sm, sc, G4);
+                                for (int i = tid; i < K; i += G4) { sm.ckey[i] = sm.skey[i]; sm.clm[i] = sm.slm[i]; sm.cbt[i] = sm.sbt[i]; }
                                 if (tid == 0) { sc.nbuf = K; sc.thr = fmaxf(sc.thr, score_of(kth)); st[kCompactions] += 1; }
-                                __syncthreads();
+                                gsync(G4);
                             }
                             const float thr2 = sc.thr;
-                            for (int q = tid; q < np; q += NT) {
+                            for (int q = tid; q < np; q += G4) {
                                 const uint32_t pq = s_pairs[q];
                                 const int a2 = (int)(pq >> 16), jq = (int)(pq & 0xffffu);
                                 const int k = sm.alive_idx[a2];
@@ -729,15 +825,16 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 st[line >= 0 ? kEvalDense : kEvalSparse] += 1;
                                 if (s > kNeg && s >= thr2) push_cand(sm, sc, make_key(s, flat_idx(k, wq)), ln, bn);
                             }
-                            __syncthreads();
+                            gsync(G4);
                             c4c = clock64();
                             if (tid == 0) { sc.npair = 0; st[kCycP4Eval] += (uint32_t)(c4c - c4e); }
-                            __syncthreads();
+                            gsync(G4);
                             if (!any_full) break;
                         }
                     }
                 }
             }
+            if (solo && helper) continue;  // heavy frame done for the helpers
 
             // ------------------------------------------------ phase 5: flat TopK + θ-prune
             const long long c2 = clock64();
@@ -746,9 +843,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const int* kl;
             const int* kb;
             int nsel;
-            if (n > NT) {
-                const uint64_t kth = radix_kth<NT>(sm.ckey, n, K, sm, sc);
-                gather_selected<NT>(n, kth, sm, sc);
+            if (n > G) {
+                const uint64_t kth = radix_kth(sm.ckey, n, K, sm, sc, G);
+                gather_selected(n, kth, sm, sc, G);
                 kk = sm.skey; kl = sm.slm; kb = sm.sbt; nsel = K;
             } else {
                 kk = sm.ckey; kl = sm.clm; kb = sm.cbt; nsel = n;
@@ -759,9 +856,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 myk = kk[tid]; myl = kl[tid]; myb = kb[tid];
                 for (int j = 0; j < nsel; ++j) rank += kk[j] > myk ? 1 : 0;
             }
-            __syncthreads();
+            gsync(G);
             if (tid < nsel && rank < K) { sm.skey[rank] = myk; sm.slm[rank] = myl; sm.sbt[rank] = myb; }
-            __syncthreads();
+            gsync(G);
             const int nkeep = nsel < K ? nsel : K;
             const float mx = nkeep > 0 ? score_of(sm.skey[0]) : kNeg;  // max_score
             const float tau = __fsub_rn(mx, p.theta);
@@ -816,7 +913,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     p.bp_label[bpo + i] = 0xffff;
                 }
             }
-            __syncthreads();
+            gsync(G);
             // ------------------------------------------------ phase 7: RecombineHypotheses
             unsigned grp = 0;
             const bool small_beam = K <= 32;  // all slots live in warp 0
@@ -930,19 +1027,19 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 }
                 sm.skey[i] = (uint64_t)__float_as_uint(s);  // stash merged score
             }
-            __syncthreads();
+            gsync(G);
             if (tid < K) nxt.acc[tid] = __uint_as_float((uint32_t)sm.skey[tid]);
-            cb ^= 1;
             if (tid == 0) {
                 const long long c4 = clock64();
                 st[kCycP13] += (uint32_t)(c1 - c0); st[kCycP4] += (uint32_t)(c2 - c1);
                 st[kCycP5] += (uint32_t)(c3 - c2); st[kCycP67] += (uint32_t)(c4 - c3);
                 if (m_frame > 0) { st[kHeavyFrames] += 1; st[kCycHeavy] += (uint32_t)(c4 - c0); }
             }
-            __syncthreads();
+            gsync(G);
         }
         cp_wait<0>();
-        const Bank cur = bank(cb);
+        __syncthreads();  // join the beam warp and the helpers (solo mode)
+        const Bank cur = bank(L & 1);
 
         // ------------------------------------------------------------ EOS + final merge (R15)
         float fs = kNeg;
@@ -990,7 +1087,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 bestkey = ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - (uint32_t)i);
             }
         }
-        bestkey = block_max_u64<NT>(bestkey, sc);
+        bestkey = block_max_u64(bestkey, sc, NT);
         const bool has_best = bestkey != 0ull;
         const int best = has_best ? (int)(0xffffffffu - (uint32_t)bestkey) : -1;
         const float best_score = has_best ? score_of(bestkey) : kNeg;
@@ -1029,7 +1126,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 cnt += (at != blank && at != ap) ? 1 : 0;
             }
         int ntok;
-        int off = block_exscan<NT>(cnt, &ntok, sc);
+        int off = block_exscan(cnt, &ntok, sc, NT);
         int32_t* otok = p.out_tokens + (int64_t)b * p.T;
         int32_t* ots = p.out_ts ? p.out_ts + (int64_t)b * p.T : nullptr;
         if (has_best)
@@ -1120,8 +1217,11 @@ int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std:
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm);
     if (e != cudaSuccess || occ < 1) { err = "occupancy query failed"; return 1; }
     const int grid = std::min(p.B, nsm * occ);
+    DecodeParams q = p;
+    const char* e_solo = getenv("FLEXCTC_SOLO");  // "0": every phase uses the whole CTA (test switch)
+    q.solo_off = (e_solo && e_solo[0] == '0') ? 1 : 0;
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-    kern<<<grid, NT, sm, st>>>(p, R, cap, nrow, dense_min);
+    kern<<<grid, NT, sm, st>>>(q, R, cap, nrow, dense_min);
     e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }

@@ -89,6 +89,7 @@ struct DecodeParams {
     float alpha_lm, alpha_bt, beta, theta;
     int32_t merge_mode, retract;
     int32_t use_lm, use_bt;
+    int32_t solo_off;     // tuning/test switch: disable the beam-warp + helpers mode
     LmDev lm;
     BoostDev bt;
     // workspace

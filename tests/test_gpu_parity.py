@@ -136,13 +136,18 @@ def test_c5_sampled(lm_pair, bt_pair):
     run_pair(D, L, wl_cfg(wl), lm_pair[0], lm_pair[1], bt_pair[0], bt_pair[1], idx=idx, ctx="c5")
 
 
-@pytest.mark.parametrize("nt,dense", [("32", "1"), ("32", None), ("64", "24"), ("128", None), ("256", "1")])
-def test_kernel_variants_c4(lm_pair, bt_pair, nt, dense, monkeypatch):
-    """Every launch variant (threads per utterance, LM row-cache dense path) is bit-identical
-    to the oracle on c4 utterances (FLEXCTC_NT / FLEXCTC_DENSE_MIN are tuning overrides)."""
+@pytest.mark.parametrize("nt,dense,solo", [("32", "1", None), ("32", None, None), ("64", "24", None),
+                                           ("128", None, None), ("256", "1", None), ("256", None, "0"),
+                                           ("256", "24", "0")])
+def test_kernel_variants_c4(lm_pair, bt_pair, nt, dense, solo, monkeypatch):
+    """Every launch variant (threads per utterance, LM row-cache dense path, beam-warp + helpers
+    mode on/off) matches the oracle on c4 utterances (FLEXCTC_NT / FLEXCTC_DENSE_MIN /
+    FLEXCTC_SOLO are tuning overrides)."""
     monkeypatch.setenv("FLEXCTC_NT", nt)
     if dense:
         monkeypatch.setenv("FLEXCTC_DENSE_MIN", dense)
+    if solo:
+        monkeypatch.setenv("FLEXCTC_SOLO", solo)
     wl, D, L, _, _ = synth.workload_inputs("c4", B=12)
     run_pair(D, L, wl_cfg(wl), lm_pair[0], lm_pair[1], bt_pair[0], bt_pair[1], ctx=f"nt{nt} dense{dense}")
 

@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 // tokens within kListDelta of it (capped at 32; the count says when it overflowed)
                 const int h = ltid;
                 if (h == 0) s_sum_cnt[slot] = 0;
+                helpers_sync(lnt);  // every helper's cp.async of row t has landed (each waited its own)
                 float bv = kNeg;
                 int bi = -1;
                 for (int w = h; w < blank; w += lnt) {

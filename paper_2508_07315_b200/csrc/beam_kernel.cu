@@ -342,6 +342,17 @@ __device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1,
     if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
 }
 
+// Pull the LM record and boost values of a candidate's next state into L1 when the candidate is
+// pushed, so that beams.update (phase 6) finds them there if the candidate is selected.
+__device__ __forceinline__ void prefetch_state(const DecodeParams& p, int ln, int bn) {
+    if (p.use_lm && ln >= 0)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.lm.rec + (size_t)ln * (p.lm.RW / 4)));
+    if (p.use_bt) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.bt.maxd + bn));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.bt.U + bn));
+    }
+}
+
 // barrier among the helper warps only (named barrier 2)
 __device__ __forceinline__ void helpers_sync(int n) { asm volatile("bar.sync 2, %0;" ::"r"(n) : "memory"); }
 
@@ -644,7 +655,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     if (sbk > kNeg && sbk >= tau0) push_cand(sm, sc, make_key(sbk, flat_idx(tid, blank)), cur.lms[tid], cur.bts[tid]);
                     if (srk > kNeg && srk >= tau0) push_cand(sm, sc, make_key(srk, flat_idx(tid, lk)), cur.lms[tid], cur.bts[tid]);
                 }
-                if (sA > kNeg && sA >= tau0) push_cand(sm, sc, make_key(sA, flat_idx(kA, wstar)), lnA, bnA);
+                if (sA > kNeg && sA >= tau0) {
+                    push_cand(sm, sc, make_key(sA, flat_idx(kA, wstar)), lnA, bnA);
+                    prefetch_state(p, lnA, bnA);
+                }
 
                 // ------------------------------------------------ phase 3 (decision): token filter
                 // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
@@ -824,7 +838,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 int ln, bn;
                                 const float s = eval(cur, k, s0, wq, ln, bn, line >= 0 ? rowval + (size_t)line * VP : nullptr);
                                 st[line >= 0 ? kEvalDense : kEvalSparse] += 1;
-                                if (s > kNeg && s >= thr2) push_cand(sm, sc, make_key(s, flat_idx(k, wq)), ln, bn);
+                                if (s > kNeg && s >= thr2) {
+                                    push_cand(sm, sc, make_key(s, flat_idx(k, wq)), ln, bn);
+                                    prefetch_state(p, ln, bn);
+                                }
                             }
                             gsync(G4);
                             c4c = clock64();

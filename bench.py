@@ -231,8 +231,8 @@ def run_flexctc(args):
     # weak scaling: rank r decodes its own batch of the workload (seed offset r)
     _, D, L, arpa, ph = synth.workload_inputs(args.workload, seed_offset=rank)
     B, T, Vp1 = D.shape
-    lm = F.LM(arpa, wl.V, device=local) if wl.lm else None
-    bt = F.Boost(ph, 1.0, wl.V, device=local) if wl.boost else None
+    lm = F.LM(arpa, wl.V, device=gpu) if wl.lm else None
+    bt = F.Boost(ph, 1.0, wl.V, device=gpu) if wl.boost else None
     cfg = F.config(wl.beam, wl.alpha_lm if wl.lm else 0.0, wl.alpha_bt if wl.boost else 0.0, wl.beta, wl.theta,
                    wl.merge_mode)
     Dd = torch.from_numpy(D).to(dev)

@@ -33,7 +33,11 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, timers: bool | None = None) -> str:
+    """timers: compile the per-phase cycle counters in (-DFLEXCTC_PHASE_TIMERS; also via the
+    FLEXCTC_PHASE_TIMERS=1 environment variable)."""
+    if timers is None:
+        timers = os.environ.get("FLEXCTC_PHASE_TIMERS") == "1"
     if not force and up_to_date():
         return LIB
     objdir = os.path.join(HERE, "build")
@@ -45,6 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                "-Xcompiler", "-ffp-contract=off", "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
+            cmd += ["-DFLEXCTC_PHASE_TIMERS"] if timers else []
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
@@ -54,4 +59,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timers=True if "--timers" in sys.argv else None))

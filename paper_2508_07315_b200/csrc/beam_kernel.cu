@@ -44,6 +44,14 @@
 namespace flexctc {
 namespace {
 
+// Per-phase SM-cycle counters (device stats words 10-22) cost ~100 instructions per frame on the
+// beam warp; they are compiled in only with -DFLEXCTC_PHASE_TIMERS (build.py --timers).
+#ifdef FLEXCTC_PHASE_TIMERS
+#define TCLK() clock64()
+#else
+#define TCLK() 0ll
+#endif
+
 constexpr float kNeg = -INFINITY;
 constexpr int kDenseMinTokens = 24;  // listed tokens per frame that switch to LM rows (when enabled)
 
@@ -434,7 +442,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
     const int RWS = lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
-    const bool solo = K <= 32 && NT > 32 && R == kRing && !p.solo_off;
+    const bool solo = K <= 32 && NT >= 128 && R == kRing && !p.solo_off;  // >= 3 helper warps
     const bool helper = solo && tid >= 32;
     const bool bw = !solo || tid < 32;               // takes part in the slot-serial phases
     const int ltid = helper ? tid - 32 : tid;        // row loader index / count
@@ -540,7 +548,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const int cb = t & 1;  // current bank (every thread tracks it, helpers included)
             const Bank cur = bank(cb);
             const Bank nxt = bank(cb ^ 1);
-            const long long ctop = clock64();
+            const long long ctop = TCLK();
             const int slot = t % R;
             float* ring_t = sm.ring + (size_t)slot * (VP + 4);
             const float* row = ring_t + row_off(Db + (int64_t)t * p.stride_t);
@@ -587,7 +595,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             }
             if (tid == 0) { sc.nbuf = 0; sc.m = 0; sc.npair = 0; }
             __syncthreads();  // B0: row t and its summary are ready
-            const long long c0 = clock64();
+            const long long c0 = TCLK();
             if (tid == 0) st[kCycTop] += (uint32_t)(c0 - ctop);
 
             const int G = solo ? 32 : NT;  // group of the slot-parallel phases
@@ -634,7 +642,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
 
                 // ------------------------------------------------ phase 2: exact candidates of the frame's
                 // best non-blank token (tightens the lower bound of the frame max on emission frames)
-                const long long cp2 = clock64();
+                const long long cp2 = TCLK();
                 float tau0 = __fsub_rn(mxrb, p.theta);
                 if (nalive > 0 && mxrb > kNeg) {
                     const float reach = __fadd_rn(__fadd_rn(accmax, dstar), ubvmax) +
@@ -662,7 +670,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
 
                 // ------------------------------------------------ phase 3 (decision): token filter
                 // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
-                const long long cp3 = clock64();
+                const long long cp3 = TCLK();
                 if (tid == 0) st[kCycP2] += (uint32_t)(cp3 - cp2);
                 bool scan = false;
                 float dthr = INFINITY;
@@ -714,13 +722,13 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 }
                 __syncthreads();
             }
-            if (tid == 0) st[kCycP3] += (uint32_t)(clock64() - c0);
+            if (tid == 0) st[kCycP3] += (uint32_t)(TCLK() - c0);
             // group of phase 4: the whole CTA when it scanned, else the beam warp alone (solo)
             const int G4 = (solo && !scan_all) ? 32 : NT;
             if (solo && helper && !scan_all) continue;  // helpers go on to the next row + summary
 
             // ------------------------------------------------ phase 4: exact non-rb candidates
-            const long long c1 = clock64();
+            const long long c1 = TCLK();
             const int m_frame = sc.m;
             {
                 const int m = m_frame;
@@ -750,16 +758,16 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         st[kRowsBuilt] += nb;
                     }
                     __syncthreads();
-                    const long long cr = clock64();
+                    const long long cr = TCLK();
                     for (int i = 0; i < s_nbuild; ++i)
                         build_lm_row<NT>(p.lm, s_build[2 * i + 1], rowval + (size_t)s_build[2 * i] * VP, V);
                     __syncthreads();
-                    if (tid == 0) st[kCycRows] += (uint32_t)(clock64() - cr);
+                    if (tid == 0) st[kCycRows] += (uint32_t)(TCLK() - cr);
                 } else if (m > 0) {
                     for (int a2 = tid; a2 < nalive; a2 += G4) s_line[a2] = -1;
                 }
                 if (m > 0) {
-                    const long long c4s = clock64();
+                    const long long c4s = TCLK();
                     // per live position: {acc, ub (β + α_LM·max P + α_BT·max Δ), |terms|, last}
                     for (int a2 = tid; a2 < nalive; a2 += G4) {
                         const int k = sm.alive_idx[a2];
@@ -778,7 +786,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         s_suf[a2] = make_float2(am, um);
                     }
                     gsync(G4);
-                    long long c4c = clock64();
+                    long long c4c = TCLK();
                     if (tid == 0) st[kCycP4Setup] += (uint32_t)(c4c - c4s);
                     // Token-major collection (lane = listed token, loop over the live slots with an
                     // early exit) of the (position, token) pairs that pass the bounds, then one
@@ -815,7 +823,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                             }
                             if (!full) a_from = nalive;
                             const int any_full = G4 == 32 ? (int)__any_sync(0xffffffffu, full) : __syncthreads_or(full);
-                            const long long c4e = clock64();
+                            const long long c4e = TCLK();
                             if (tid == 0) st[kCycP4Collect] += (uint32_t)(c4e - c4c);
                             const int np = min(sc.npair, kPairCap);
                             if (sc.nbuf > cap - np) {
@@ -844,7 +852,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 }
                             }
                             gsync(G4);
-                            c4c = clock64();
+                            c4c = TCLK();
                             if (tid == 0) { sc.npair = 0; st[kCycP4Eval] += (uint32_t)(c4c - c4e); }
                             gsync(G4);
                             if (!any_full) break;
@@ -855,7 +863,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             if (solo && helper) continue;  // heavy frame done for the helpers
 
             // ------------------------------------------------ phase 5: flat TopK + θ-prune
-            const long long c2 = clock64();
+            const long long c2 = TCLK();
             const int n = sc.nbuf;
             const uint64_t* kk;
             const int* kl;
@@ -881,7 +889,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const float mx = nkeep > 0 ? score_of(sm.skey[0]) : kNeg;  // max_score
             const float tau = __fsub_rn(mx, p.theta);
 
-            const long long c3 = clock64();
+            const long long c3 = TCLK();
             // ------------------------------------------------ phase 6: beams.update into nxt
             const int64_t bpo = ((int64_t)b * p.T + t) * K;
             bool live = false, emit = false;
@@ -1048,7 +1056,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             gsync(G);
             if (tid < K) nxt.acc[tid] = __uint_as_float((uint32_t)sm.skey[tid]);
             if (tid == 0) {
-                const long long c4 = clock64();
+                const long long c4 = TCLK();
                 st[kCycP13] += (uint32_t)(c1 - c0); st[kCycP4] += (uint32_t)(c2 - c1);
                 st[kCycP5] += (uint32_t)(c3 - c2); st[kCycP67] += (uint32_t)(c4 - c3);
                 if (m_frame > 0) { st[kHeavyFrames] += 1; st[kCycHeavy] += (uint32_t)(c4 - c0); }
@@ -1200,50 +1208,115 @@ size_t smem_bytes(int K, int Vp1, int R, int cap, int nch, int RWS) {
     return s;
 }
 
+struct Plan {
+    size_t sm = 0;
+    int nrow = 0, occ = 0, R = 4, cap = 0, dense_min = kDenseMinTokens;
+};
+
+// Shared-memory layout, row-cache lines and occupancy of the NT-thread kernel for this decode.
 template <int NT, int LMV>
-int launch_nt(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
+int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
     const int VP = (p.Vp1 + 3) & ~3;
-    const int R = VP <= 2048 ? 4 : 2;
-    const int cap = 4 * NT;  // >= 3K phase-1/2 pushes, and >= kPairCap + K for phase 4
+    pl.R = VP <= 2048 ? 4 : 2;
+    pl.cap = 4 * NT;  // >= 3K phase-1/2 pushes, and >= kPairCap + K for phase 4
     const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
-    size_t sm = smem_bytes(p.K, p.Vp1, R, cap, p.nch, RWS) + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) + 16 : 0);
-    if (sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
-    // LM row cache: as many lines as fit the shared memory left at the register-limited
-    // occupancy (CTAs / SM), at most min(K, 32)
-    int nrow = 0;
+    pl.sm = smem_bytes(p.K, p.Vp1, pl.R, pl.cap, p.nch, RWS) + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) + 16 : 0);
+    if (pl.sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
     auto kern = ctc_beam_kernel<NT, LMV>;
     cudaFuncAttributes fattr{};
     cudaFuncGetAttributes(&fattr, kern);
     // The dense-frame LM row cache is off by default: with 8 warps per utterance the batched
-    // sparse evaluation is faster on c3-c5 (measured); FLEXCTC_DENSE_MIN=<tokens> enables it.
-    int dense_min = kDenseMinTokens;
+    // sparse evaluation is faster on c3-c5 (measured); FLEXCTC_DENSE_MIN=<tokens> enables it, with
+    // as many lines as fit the shared memory left at the register-limited occupancy (<= min(K, 32)).
     const char* e_dm = getenv("FLEXCTC_DENSE_MIN");
-    if (e_dm) dense_min = std::max(1, atoi(e_dm));
+    if (e_dm) pl.dense_min = std::max(1, atoi(e_dm));
+    pl.nrow = 0;
     if (p.use_lm && e_dm) {
         const size_t line = 4 * (size_t)VP + 4;
         const int occ_regs = std::max(1, 65536 / std::max(1, fattr.numRegs * NT));
         const size_t per_cta = std::min<size_t>(200 * 1024, (size_t)(224 * 1024) / (size_t)occ_regs);
         const size_t budget = per_cta - std::min<size_t>(fattr.sharedSizeBytes, per_cta / 2);
-        if (sm + 16 < budget) nrow = (int)std::min<size_t>((budget - sm - 16) / line, (size_t)std::min(p.K, 32));
-        sm += nrow ? 4 * (size_t)nrow * VP + ((4 * (size_t)nrow + 15) & ~size_t(15)) : 0;
+        if (pl.sm + 16 < budget) pl.nrow = (int)std::min<size_t>((budget - pl.sm - 16) / line, (size_t)std::min(p.K, 32));
+        pl.sm += pl.nrow ? 4 * (size_t)pl.nrow * VP + ((4 * (size_t)pl.nrow + 15) & ~size_t(15)) : 0;
     }
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm);
-    if (e != cudaSuccess || occ < 1) { err = "occupancy query failed"; return 1; }
-    const int grid = std::min(p.B, nsm * occ);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.occ, kern, NT, pl.sm);
+    if (e != cudaSuccess || pl.occ < 1) { err = "occupancy query failed"; return 1; }
+    return 0;
+}
+
+template <int NT, int LMV>
+int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
+    auto kern = ctc_beam_kernel<NT, LMV>;
+    const int grid = std::min(p.B, nsm * pl.occ);
     DecodeParams q = p;
     const char* e_solo = getenv("FLEXCTC_SOLO");  // "0": every phase uses the whole CTA (test switch)
     q.solo_off = (e_solo && e_solo[0] == '0') ? 1 : 0;
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-    kern<<<grid, NT, sm, st>>>(q, R, cap, nrow, dense_min);
-    e = cudaGetLastError();
+    kern<<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+    cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     return 0;
+}
+
+template <int LMV>
+int plan_any(int nt, const DecodeParams& p, Plan& pl, std::string& err) {
+    switch (nt) {
+        case 32: return plan_nt<32, LMV>(p, pl, err);
+        case 64: return plan_nt<64, LMV>(p, pl, err);
+        case 128: return plan_nt<128, LMV>(p, pl, err);
+        default: return plan_nt<256, LMV>(p, pl, err);
+    }
+}
+template <int LMV>
+int run_any(int nt, const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
+    switch (nt) {
+        case 32: return run_nt<32, LMV>(p, pl, nsm, st, ev0, ev1, err);
+        case 64: return run_nt<64, LMV>(p, pl, nsm, st, ev0, ev1, err);
+        case 128: return run_nt<128, LMV>(p, pl, nsm, st, ev0, ev1, err);
+        default: return run_nt<256, LMV>(p, pl, nsm, st, ev0, ev1, err);
+    }
+}
+
+// Relative per-utterance latency of the NT-thread kernel (measured on c4 / c5, round 1): more
+// warps shorten each frame step; fewer warps fit more utterances per SM.
+double latency_factor(int nt, int K) {
+    if (K <= 32) return nt == 32 ? 1.75 : nt == 64 ? 1.5 : nt == 128 ? 1.2 : 1.0;
+    return nt == 64 ? 1.6 : nt == 128 ? 1.3 : 1.0;
+}
+
+template <int LMV>
+int launch_lmv(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int need = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
+    int forced = 0;
+    if (const char* e_nt = getenv("FLEXCTC_NT")) {  // tuning override (never below the beam)
+        const int want = atoi(e_nt);
+        if ((want == 32 || want == 64 || want == 128 || want == 256) && want >= need) forced = want;
+    }
+    // Threads per utterance: 8 warps (shortest frame step) unless the batch is much larger than
+    // the GPU (B > 4 x #SMs), where (waves of utterances) x (per-utterance latency) is minimised.
+    // Below that, the longest utterance dominates (LPT queue), so latency wins (c5: B = 512).
+    int best_nt = 256;
+    Plan best;
+    double best_cost = 1e300;
+    const bool throughput = p.B > 4 * nsm;
+    for (int nt = need; nt <= 256; nt *= 2) {
+        if (forced && nt != forced) continue;
+        if (!forced && !throughput && nt != 256) continue;
+        Plan pl;
+        const int rc = plan_any<LMV>(nt, p, pl, err);
+        if (rc) { if (forced || nt == 256) return rc; continue; }
+        const double waves = std::ceil((double)p.B / ((double)nsm * pl.occ));
+        const double cost = waves * latency_factor(nt, p.K);
+        if (cost < best_cost - 1e-9 || (cost < best_cost + 1e-9 && nt > best_nt)) { best_cost = cost; best_nt = nt; best = pl; }
+    }
+    if (best_cost >= 1e299) return 2;
+    return run_any<LMV>(best_nt, p, best, nsm, st, ev0, ev1, err);
 }
 
 }  // namespace
@@ -1256,21 +1329,8 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
     order_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p.lengths, p.B, p.T, p.order, p.len_c, p.flags, p.B <= 16384);
     e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-    // 8 warps per utterance: the frame scans, the pair collection/evaluation and the selection
-    // parallelise over tokens, which shortens the latency-bound frame step (measured on c2-c5)
-    int nt = 256;
-    if (const char* e_nt = getenv("FLEXCTC_NT")) {  // tuning override (never below the beam)
-        const int want = atoi(e_nt);
-        const int need = p.K <= 32 ? 32 : p.K <= 64 ? 64 : p.K <= 128 ? 128 : 256;
-        if ((want == 32 || want == 64 || want == 128 || want == 256) && want >= need) nt = want;
-    }
     const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
-    switch (nt) {
-        case 32: return small_lm ? launch_nt<32, 2>(p, st, ev0, ev1, err) : launch_nt<32, kMaxLmLevels>(p, st, ev0, ev1, err);
-        case 64: return small_lm ? launch_nt<64, 2>(p, st, ev0, ev1, err) : launch_nt<64, kMaxLmLevels>(p, st, ev0, ev1, err);
-        case 128: return small_lm ? launch_nt<128, 2>(p, st, ev0, ev1, err) : launch_nt<128, kMaxLmLevels>(p, st, ev0, ev1, err);
-        default: return small_lm ? launch_nt<256, 2>(p, st, ev0, ev1, err) : launch_nt<256, kMaxLmLevels>(p, st, ev0, ev1, err);
-    }
+    return small_lm ? launch_lmv<2>(p, st, ev0, ev1, err) : launch_lmv<kMaxLmLevels>(p, st, ev0, ev1, err);
 }
 
 }  // namespace flexctc

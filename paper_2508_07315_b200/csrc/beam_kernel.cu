@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         const int b = p.order[u];
         const int L = p.len_c[b];
         const float* Db = p.log_probs + (int64_t)b * p.stride_b;
+        const int64_t bp_base = (int64_t)b * p.T * K;  // backpointers of this utterance
 
         // ------------------------------------------------------------ init (Alg. 1)
         {
@@ -891,7 +892,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
 
             const long long c3 = TCLK();
             // ------------------------------------------------ phase 6: beams.update into nxt
-            const int64_t bpo = ((int64_t)b * p.T + t) * K;
+            const int64_t bpo = bp_base + (int64_t)(t * K);
             bool live = false, emit = false;
             int par = 0;
             int4 rec_ld[kRec / 4];
@@ -935,8 +936,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     nxt.last[i] = blank;
                     nxt.hash[i] = 0ull;
                     nxt.lms[i] = 0; nxt.bts[i] = 0; nxt.anc[i] = 0;
-                    p.bp_parent[bpo + i] = 0xff;
-                    p.bp_label[bpo + i] = 0xffff;
+                    // dead slots need no backpointer: the backtrace only follows live ancestors
                 }
             }
             gsync(G);

@@ -114,6 +114,14 @@ def test_c2_beam_vs_greedy():
         assert np.float32(g["scores"][b]) == np.float32(score)
 
 
+def test_fused_greedy_c4(lm_pair, bt_pair):
+    """K = 1 with LM + boosting: the fused greedy decoder of PAPER Table II ('greedy' + LM/PB)."""
+    wl, D, L, _, _ = synth.workload_inputs("c4")
+    for mode in (0, 1):
+        run_pair(D, L, wl_cfg(wl, beam=1, merge_mode=mode), lm_pair[0], lm_pair[1], bt_pair[0], bt_pair[1],
+                 ctx=f"greedy-fused m{mode}")
+
+
 def test_c3_full(lm_pair):
     wl, D, L, _, _ = synth.workload_inputs("c3")
     run_pair(D, L, wl_cfg(wl), glm=lm_pair[0], olm=lm_pair[1], ctx="c3")

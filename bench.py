@@ -325,9 +325,12 @@ def run_flexctc(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": frames_all * synth.FRAME_SECONDS * args.steps / float(te[0]), "unit": UNIT,
-               "h2d_bytes_per_step": int(D.nbytes + L.nbytes),
+               # the streamed path (K > 1) copies only the valid frames t < L_b
+               "h2d_bytes_per_step": int((int(np.clip(L, 0, T).sum()) * Vp1 * 4 if cfg.beam > 1 else D.nbytes)
+                                         + L.nbytes),
                "d2h_bytes_per_step": int(B * T * 4 * 2 + B * 4 * 2),
-               "path": "flexctc_decode_host (pinned host buffers, copies + decode + sync inside)"}
+               "path": "flexctc_decode_host (pinned host buffers; H2D in frame chunks overlapping the decode, "
+                       "D2H and sync inside)"}
 
     # gather the final results (the only cross-GPU traffic)
     gathered = None

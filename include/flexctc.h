@@ -47,6 +47,8 @@ typedef enum {
 /* Device-side flags reported by flexctc_check (bitwise OR). */
 #define FLEXCTC_FLAG_LENGTH_CLAMPED_HIGH 1u /* some lengths[b] > T: clamped to T  */
 #define FLEXCTC_FLAG_LENGTH_CLAMPED_LOW 2u  /* some lengths[b] < 0: clamped to 0  */
+#define FLEXCTC_FLAG_STREAM_TIMEOUT 4u      /* flexctc_decode_host: a frame chunk never arrived
+                                               (10 s watchdog); the outputs are invalid        */
 
 const char* flexctc_last_error(void);
 const char* flexctc_version(void);
@@ -170,8 +172,19 @@ flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags);
  * lengths to the device (into `device_scratch`, which must hold
  * flexctc_host_scratch_bytes(B, T, Vp1, cfg) bytes of device memory), decodes, copies the
  * outputs back into host arrays and synchronises `stream`. Pinned host memory makes the
- * copies asynchronous DMA. Outputs as flexctc_decode, in host memory. */
+ * copies asynchronous DMA. Outputs as flexctc_decode, in host memory.
+ * For K > 1 the input is streamed: the beam kernel is launched first and frame chunks
+ * [t0, t1) of every utterance (only frames t < lengths[b]) are copied on a library-owned copy
+ * stream, each followed by a "frames ready" word the row loaders wait on, so the copy overlaps
+ * the frame recurrence (flexctc_host_streaming() says whether this is active). The host
+ * buffers must stay unchanged until the call returns. A chunk that never lands (a failed copy)
+ * releases the kernel after 10 s with FLEXCTC_FLAG_STREAM_TIMEOUT (flexctc_check). */
 size_t flexctc_host_scratch_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg);
+/* 1 if flexctc_decode_host on the current device streams its input (frame chunks copied on a
+ * library-owned copy stream while the beam kernel runs, each chunk signalled by a stream memory
+ * operation), 0 if it copies everything before decoding (K = 1, no stream memory operations,
+ * or the FLEXCTC_NO_STREAM_INPUT environment switch). */
+int32_t flexctc_host_streaming(void);
 flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* lengths_host,
                                    int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg,
                                    const flexctc_lm* lm, const flexctc_boost* boost,

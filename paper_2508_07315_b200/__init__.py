@@ -2,4 +2,4 @@
 n-gram shallow fusion and Aho-Corasick phrase boosting, as hand-written sm_100a CUDA behind a
 C ABI (include/flexctc.h). See DESIGN.md."""
 from .flexctc import (LM, Boost, Config, FlexCTCError, check, config, decode, decode_host, stats,  # noqa: F401
-                      host_scratch_bytes, make_workspace, version, workspace_bytes)
+                      host_scratch_bytes, host_streaming, make_workspace, version, workspace_bytes)

@@ -1,6 +1,7 @@
 // C ABI of libflexctc (include/flexctc.h): validation, handle management, device upload,
 // workspace layout, and the two launches of a decode. No compute happens on the host: the
 // builders only lay out the LM / boost tables, and flexctc_decode refuses host memory.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -254,11 +255,14 @@ static flexctc_status validate_cfg(const flexctc_config* cfg) {
     return FLEXCTC_OK;
 }
 
-flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lengths,
-                              int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
-                              const flexctc_boost* boost, void* workspace, size_t workspace_bytes,
-                              flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
-                              float* out_scores, int32_t* out_timestamps, int32_t* out_alignment) {
+// flexctc_decode plus the streamed-input fields of DecodeParams (ready, overread), which only
+// flexctc_decode_host sets.
+static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lengths,
+                                  int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
+                                  const flexctc_boost* boost, void* workspace, size_t workspace_bytes,
+                                  flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                                  float* out_scores, int32_t* out_timestamps, int32_t* out_alignment,
+                                  const uint32_t* ready, int overread) {
     flexctc_status st = validate_cfg(cfg);
     if (st != FLEXCTC_OK) return st;
     if (B < 0 || T < 0) return fail(FLEXCTC_ERR_INVALID_ARG, "B and T must be >= 0");
@@ -308,11 +312,22 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
     p.nch = wl.nch;
     p.out_tokens = out_tokens; p.out_num = out_num_tokens; p.out_scores = out_scores;
     p.out_ts = out_timestamps; p.out_align = out_alignment;
+    p.ready = ready;
+    p.overread = overread;
     std::string err;
     int rc = launch_decode(p, (void*)stream, g_ev_start, g_ev_stop, err);
     if (rc == 2) return fail(FLEXCTC_ERR_CAPACITY, err);
     if (rc != 0) return fail(FLEXCTC_ERR_CUDA, err);
     return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lengths,
+                              int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
+                              const flexctc_boost* boost, void* workspace, size_t workspace_bytes,
+                              flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                              float* out_scores, int32_t* out_timestamps, int32_t* out_alignment) {
+    return decode_impl(log_probs, stride_b, stride_t, lengths, B, T, Vp1, cfg, lm, boost, workspace, workspace_bytes,
+                       stream, out_tokens, out_num_tokens, out_scores, out_timestamps, out_alignment, nullptr, 0);
 }
 
 void flexctc_set_profile_events(void* ev_start, void* ev_stop) {
@@ -337,10 +352,73 @@ flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags) {
 
 size_t flexctc_host_scratch_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg) {
     if (!cfg || B < 0 || T < 0 || Vp1 < 2 || cfg->beam < 1) return 0;
-    size_t s = align256((size_t)B * T * Vp1 * 4) + align256((size_t)B * 4);
+    size_t s = align256((size_t)B * T * Vp1 * 4 + 16) + align256((size_t)B * 4) + 256;
     s += align256((size_t)B * T * 4) * 2 + align256((size_t)B * 4) * 2;
     s += workspace_layout(B, T, cfg->beam).total;
     return s;
+}
+
+}  // extern "C"
+
+namespace flexctc {
+namespace {
+
+// Per-thread resources of the streamed host path: a non-blocking copy stream, two events, and
+// cuStreamWriteValue32 (a stream memory operation: the front end writes the "frames ready"
+// word after each chunk's copy without occupying an SM, so it cannot be starved by the
+// persistent kernel). Resolved through the runtime, no link against libcuda.
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct HostPath {
+    int device = -1;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    WriteValue32Fn write32 = nullptr;
+    bool memops = false;
+};
+thread_local HostPath g_host;
+
+bool host_path_init(int dev) {
+    if (g_host.device == dev) return g_host.memops;
+    g_host = HostPath{};
+    g_host.device = dev;
+    if (cudaStreamCreateWithFlags(&g_host.copy, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_host.ev_a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_host.ev_b, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn) {
+        g_host.write32 = (WriteValue32Fn)fn;
+        g_host.memops = true;  // 32-bit stream memory operations are always supported (CUDA >= 12)
+    }
+    cudaGetLastError();
+    return g_host.memops;
+}
+
+// Frame chunks of the streamed copy: small first chunks so the decode starts early, then 32.
+std::vector<int> chunk_ends(int T) {
+    std::vector<int> e;
+    int t = 0, c = 4;
+    while (t < T) {
+        t = std::min(T, t + c);
+        e.push_back(t);
+        c = std::min(32, 2 * c);
+    }
+    return e;
+}
+
+}  // namespace
+}  // namespace flexctc
+
+extern "C" {
+
+int32_t flexctc_host_streaming(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return host_path_init(dev) && !getenv("FLEXCTC_NO_STREAM_INPUT") ? 1 : 0;
 }
 
 flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* lengths_host, int32_t B, int32_t T,
@@ -356,23 +434,100 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
     if (!log_probs_host || !lengths_host || !out_tokens || !out_num_tokens || !out_scores)
         return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
     if (B == 0) return FLEXCTC_OK;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     cudaStream_t s = (cudaStream_t)stream;
-    char* d = (char*)device_scratch;
+    char* d = (char*)(((uintptr_t)device_scratch + 255) & ~(uintptr_t)255);
     size_t o = 0;
-    float* dD = (float*)(d + o); o += align256((size_t)B * T * Vp1 * 4);
+    float* dD = (float*)(d + o); o += align256((size_t)B * T * Vp1 * 4 + 16);  // + 16 B slack (overread)
     int32_t* dL = (int32_t*)(d + o); o += align256((size_t)B * 4);
     int32_t* dTok = (int32_t*)(d + o); o += align256((size_t)B * T * 4);
     int32_t* dTs = (int32_t*)(d + o); o += align256((size_t)B * T * 4);
     int32_t* dN = (int32_t*)(d + o); o += align256((size_t)B * 4);
     float* dS = (float*)(d + o); o += align256((size_t)B * 4);
     void* ws = d + o;
-    const size_t wsb = scratch_bytes - o;
-    cudaError_t e = cudaMemcpyAsync(dD, log_probs_host, (size_t)B * T * Vp1 * 4, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dL, lengths_host, (size_t)B * 4, cudaMemcpyHostToDevice, s);
+    const size_t wsb = scratch_bytes - (size_t)(d - (char*)device_scratch) - o;
+    const WorkspaceLayout wl = workspace_layout(B, T, cfg->beam);
+    // Streamed input: the persistent beam kernel starts at once and each row loader waits for
+    // its frame chunk (a "frames ready" word in the workspace, written by the copy stream after
+    // every chunk), so the host->device copy overlaps the frame recurrence. Only frames
+    // t < lengths[b] are copied (the padding is never read). K = 1 and configurations without
+    // stream memory operations copy everything first.
+    const bool streamed = host_path_init(dev) && cfg->beam > 1 && T > 0 &&
+                          !getenv("FLEXCTC_NO_STREAM_INPUT");  // test switch: copy everything, then decode
+    e = cudaMemcpyAsync(dL, lengths_host, (size_t)B * 4, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
-    st = flexctc_decode(dD, (int64_t)T * Vp1, Vp1, dL, B, T, Vp1, cfg, lm, boost, ws, wsb, stream, dTok, dN, dS,
-                        out_timestamps ? dTs : nullptr, nullptr);
-    if (st != FLEXCTC_OK) return st;
+    uint32_t* ready = nullptr;
+    if (streamed) {
+        ready = (uint32_t*)((char*)ws + wl.flags + 64 + 8 * kStatsWords);
+        e = cudaMemsetAsync(ready, 0, 4, s);
+        if (e == cudaSuccess) e = cudaEventRecord(g_host.ev_a, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(g_host.copy, g_host.ev_a, 0);
+        if (e != cudaSuccess) return cuda_fail(e, "stream setup");
+    } else {
+        e = cudaMemcpyAsync(dD, log_probs_host, (size_t)B * T * Vp1 * 4, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+    }
+    st = decode_impl(dD, (int64_t)T * Vp1, Vp1, dL, B, T, Vp1, cfg, lm, boost, ws, wsb, stream, dTok, dN, dS,
+                     out_timestamps ? dTs : nullptr, nullptr, ready, 1);
+    if (st != FLEXCTC_OK) {
+        if (streamed) cudaStreamSynchronize(s);
+        return st;
+    }
+    if (streamed) {
+        // chunk c: frames [t0, t1) of every utterance with L_b > t0 (rows of one utterance are
+        // contiguous), then ready = t1
+        const size_t row = (size_t)Vp1 * 4;
+        int Lmin = T;
+        for (int b = 0; b < B; ++b) Lmin = std::min(Lmin, std::min(std::max(lengths_host[b], 0), T));
+        std::vector<void*> dsts, srcs;
+        std::vector<size_t> sizes;
+        int t0 = 0;
+        for (int t1 : chunk_ends(T)) {
+            if (t1 <= Lmin) {  // every utterance needs the whole chunk: one 2D copy
+                e = cudaMemcpy2DAsync(dD + (size_t)t0 * Vp1, (size_t)T * row, log_probs_host + (size_t)t0 * Vp1,
+                                      (size_t)T * row, row * (size_t)(t1 - t0), (size_t)B, cudaMemcpyHostToDevice,
+                                      g_host.copy);
+            } else {  // ragged: one batched copy of the valid frames of each utterance
+                dsts.clear(); srcs.clear(); sizes.clear();
+                for (int b = 0; b < B; ++b) {
+                    const int L = std::min(std::max(lengths_host[b], 0), T);
+                    if (L <= t0) continue;
+                    const size_t off = ((size_t)b * T + t0) * Vp1;
+                    dsts.push_back(dD + off);
+                    srcs.push_back((void*)(log_probs_host + off));
+                    sizes.push_back(row * (size_t)(std::min(L, t1) - t0));
+                }
+                if (!dsts.empty()) {
+                    cudaMemcpyAttributes at{};
+                    at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+                    at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+                    size_t ai = 0, fi = 0;
+                    e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &at, &ai, 1, &fi,
+                                             g_host.copy);
+                    if (e != cudaSuccess) {  // runtime without batched copies: one copy per utterance
+                        cudaGetLastError();
+                        e = cudaSuccess;
+                        for (size_t i = 0; i < dsts.size() && e == cudaSuccess; ++i)
+                            e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, g_host.copy);
+                    }
+                }
+            }
+            if (e == cudaSuccess &&
+                g_host.write32((CUstream)g_host.copy, (CUdeviceptr)ready, (cuuint32_t)t1, 0) != CUDA_SUCCESS)
+                e = cudaErrorUnknown;
+            if (e != cudaSuccess) break;
+            t0 = t1;
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(g_host.ev_b, g_host.copy);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, g_host.ev_b, 0);
+        if (e != cudaSuccess) {
+            // the kernel may be waiting on chunks that will never come: its watchdog releases it
+            cudaStreamSynchronize(s);
+            return cuda_fail(e, "streamed H2D copy");
+        }
+    }
     e = cudaMemcpyAsync(out_tokens, dTok, (size_t)B * T * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_num_tokens, dN, (size_t)B * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_scores, dS, (size_t)B * 4, cudaMemcpyDeviceToHost, s);

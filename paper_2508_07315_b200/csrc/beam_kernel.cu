@@ -339,8 +339,16 @@ __device__ __forceinline__ void push_cand(Shared& sm, Scalars& sc, uint64_t key,
 __device__ __forceinline__ int row_off(const float* src) { return (int)(((uintptr_t)src >> 2) & 3); }
 
 // issued by `nt` threads with local index `tid` (all threads, or the helper warps)
-__device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1, int tid, int nt) {
+// overread: the buffer is library-owned (16-B aligned, >= 16 B of slack after the last row), so
+// the row is covered by whole 16-B blocks, the neighbouring rows' bytes landing unused in the slot.
+__device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1, int tid, int nt, int overread) {
     const int off = row_off(src);
+    if (overread) {
+        const float* g = src - off;
+        const int n16 = (off + Vp1 + 3) >> 2;
+        for (int i = tid; i < n16; i += nt) cp_async16(slot + 4 * i, g + 4 * i);
+        return;
+    }
     float* dst = slot + off;
     const int h = min((4 - off) & 3, Vp1);
     if (tid < h) cp_async4(dst + tid, src + tid);
@@ -348,6 +356,26 @@ __device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1,
     for (int i = tid; i < n4; i += nt) cp_async16(dst + h + 4 * i, src + h + 4 * i);
     const int t0 = h + 4 * n4;
     if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
+}
+
+// Streamed input (flexctc_decode_host): wait until frame r of every utterance has landed.
+// `ready` caches the last value seen by this thread (frames only ever become ready). A 10 s
+// watchdog flags FLEXCTC_FLAG_STREAM_TIMEOUT instead of hanging the device.
+__device__ __forceinline__ void wait_ready(const DecodeParams& p, int r, int& ready) {
+    if (!p.ready || r < ready) return;
+    const long long t0 = clock64();
+    uint32_t v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready) : "memory");
+        if ((int)v > r) break;
+        if (clock64() - t0 > 20000000000ll) {
+            atomicOr(p.flags, FLEXCTC_FLAG_STREAM_TIMEOUT);
+            v = 0x7fffffffu;
+            break;
+        }
+        __nanosleep(200);
+    }
+    ready = (int)v;
 }
 
 // Pull the LM record and boost values of a candidate's next state into L1 when the candidate is
@@ -448,6 +476,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const int ltid = helper ? tid - 32 : tid;        // row loader index / count
     const int lnt = solo ? NT - 32 : NT;
     uint32_t st[kNumStats] = {};
+    int ready = 0;  // streamed input: frames known to have landed (wait_ready)
 
     Shared sm;
     float* rowval = nullptr;  // [nrow][VP] LM rows (row cache)
@@ -541,7 +570,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         const int pf = solo ? 2 : R - 1;
         if (!solo || helper)
             for (int r = 0; r < pf; ++r) {  // prologue
-                if (r < L) load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt);
+                if (r < L) {
+                    wait_ready(p, r, ready);
+                    load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                }
                 cp_commit();
             }
 
@@ -555,7 +587,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const float* row = ring_t + row_off(Db + (int64_t)t * p.stride_t);
             if (!solo || helper) {
                 const int r = t + pf;
-                if (r < L) load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt);
+                if (r < L) {
+                    wait_ready(p, r, ready);
+                    load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                }
                 cp_commit();
                 if (solo) cp_wait<2>(); else if (R == 4) cp_wait<3>(); else cp_wait<1>();
             }

@@ -90,6 +90,13 @@ struct DecodeParams {
     int32_t merge_mode, retract;
     int32_t use_lm, use_bt;
     int32_t solo_off;     // tuning/test switch: disable the beam-warp + helpers mode
+    // streamed input (flexctc_decode_host): frames [0, *ready) of every utterance have landed in
+    // log_probs; the row loaders poll it (ld.acquire) before issuing a row. NULL = all resident.
+    const uint32_t* ready;
+    // log_probs is a library-owned buffer with >= 16 B of slack on both sides of every row, so
+    // rows are copied as whole 16-B blocks (no 4-B .ca copies that could cache stale sectors
+    // while a chunk is still in flight)
+    int32_t overread;
     LmDev lm;
     BoostDev bt;
     // workspace

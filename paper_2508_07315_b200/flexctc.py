@@ -51,7 +51,7 @@ EXPORTS = [
     "flexctc_last_error", "flexctc_version", "flexctc_lm_load", "flexctc_lm_free", "flexctc_lm_get_info",
     "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
     "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
-    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_set_profile_events", "flexctc_get_stats",
+    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_set_profile_events", "flexctc_get_stats",
 ]
 STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
               "exact_dense", "compactions", "top_token_stages", "deferred_next",
@@ -62,8 +62,8 @@ STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_f
 
 def _load() -> ctypes.CDLL:
     path = _build.LIB
-    if not os.path.exists(path):
-        _build.build()  # nvcc is part of the image; a failure here raises loudly
+    if not _build.up_to_date():
+        _build.build()  # missing or stale (sources newer); nvcc is part of the image, failures raise
     L = ctypes.CDLL(path)
     vp, i32, i64, f32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
     P = ctypes.POINTER
@@ -87,6 +87,8 @@ def _load() -> ctypes.CDLL:
     L.flexctc_host_scratch_bytes.argtypes = [i32, i32, i32, P(Config)]
     L.flexctc_host_scratch_bytes.restype = sz
     L.flexctc_decode_host.argtypes = [vp, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, vp, vp, vp, vp]
+    L.flexctc_host_streaming.argtypes = []
+    L.flexctc_host_streaming.restype = i32
     L.flexctc_set_profile_events.argtypes = [vp, vp]
     L.flexctc_set_profile_events.restype = None
     L.flexctc_get_stats.argtypes = [vp, vp, i32]
@@ -255,6 +257,11 @@ def check(workspace: Workspace) -> int:
 
 def host_scratch_bytes(B: int, T: int, Vp1: int, cfg: Config) -> int:
     return int(lib.flexctc_host_scratch_bytes(int(B), int(T), int(Vp1), ctypes.byref(cfg)))
+
+
+def host_streaming() -> bool:
+    """flexctc_host_streaming: does decode_host overlap its H2D copy with the decode here?"""
+    return bool(lib.flexctc_host_streaming())
 
 
 def decode_host(log_probs: np.ndarray, lengths: np.ndarray, cfg: Config, lm: LM | None = None,

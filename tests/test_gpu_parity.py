@@ -295,15 +295,28 @@ def test_empty_batch_and_zero_lengths(lm_pair):
     assert out["tokens"].shape == (0, 3)
 
 
-def test_decode_host_end_to_end(lm_pair, bt_pair):
-    wl, D, L, _, _ = synth.workload_inputs("c4", B=8)
-    cfg = wl_cfg(wl)
+@pytest.mark.parametrize("streamed", [True, False])
+@pytest.mark.parametrize("wname,B", [("c4", 8), ("c5", 24), ("c1", 1)])
+def test_decode_host_end_to_end(lm_pair, bt_pair, wname, B, streamed, monkeypatch):
+    """flexctc_decode_host (H2D in frame chunks overlapping the persistent kernel, or copy-then-
+    decode) returns exactly what flexctc_decode returns on the same inputs: fixed lengths (2D
+    chunk copies), ragged LibriSpeech-shaped lengths (batched per-utterance copies), tiny c1."""
+    if not streamed:
+        monkeypatch.setenv("FLEXCTC_NO_STREAM_INPUT", "1")
+    assert F.host_streaming() == streamed  # the B200 image supports stream memory operations
+    wl, D, L, _, _ = synth.workload_inputs(wname, B=B)
+    cfg = wl_cfg(wl, beam=min(wl.beam, 16))
+    glm = lm_pair[0] if wl.lm else None
+    gbt = bt_pair[0] if wl.boost else None
     Dp = torch.from_numpy(np.ascontiguousarray(D)).pin_memory()
     Lp = torch.from_numpy(L.astype(np.int32)).pin_memory()
-    out = F.decode_host(Dp, Lp, cfg, lm_pair[0], bt_pair[0])
-    g = gpu_decode(D, L, cfg, lm_pair[0], bt_pair[0])
-    assert np.array_equal(out["tokens"].numpy(), g["tokens"])
-    assert np.array_equal(out["scores"].numpy().view(np.int32), g["scores"].view(np.int32))
+    for _ in range(2):  # the second call reuses the per-thread copy stream
+        out = F.decode_host(Dp, Lp, cfg, glm, gbt)
+        g = gpu_decode(D, L, cfg, glm, gbt)
+        assert np.array_equal(out["num_tokens"].numpy(), g["num_tokens"])
+        assert np.array_equal(out["tokens"].numpy(), g["tokens"])
+        assert np.array_equal(out["timestamps"].numpy(), g["timestamps"])
+        assert np.array_equal(out["scores"].numpy().view(np.int32), g["scores"].view(np.int32))
 
 
 def test_decode_refuses_host_memory_through_abi():

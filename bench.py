@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import argparse
 import datetime
+import dataclasses
 import json
 import os
 import statistics
@@ -40,6 +41,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c4", choices=sorted(synth.WORKLOADS))
     ap.add_argument("--impl", default="flexctc", choices=["flexctc", "reference"])
+    ap.add_argument("--batch", type=int, default=0, help="override the workload's batch per GPU")
+    ap.add_argument("--beam", type=int, default=0,
+                    help="override the workload's beam (1 = the greedy kernels, SURVEY §8(f) NEXT 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0 = auto)")
@@ -228,8 +232,10 @@ def run_flexctc(args):
         else:
             dist.init_process_group(backend)
     wl = synth.WORKLOADS[args.workload]
+    if args.beam:
+        wl = dataclasses.replace(wl, beam=args.beam, name=f"{wl.name} (beam {args.beam})")
     # weak scaling: rank r decodes its own batch of the workload (seed offset r)
-    _, D, L, arpa, ph = synth.workload_inputs(args.workload, seed_offset=rank)
+    _, D, L, arpa, ph = synth.workload_inputs(args.workload, B=args.batch or None, seed_offset=rank)
     B, T, Vp1 = D.shape
     lm = F.LM(arpa, wl.V, device=gpu) if wl.lm else None
     bt = F.Boost(ph, 1.0, wl.V, device=gpu) if wl.boost else None
@@ -294,13 +300,24 @@ def run_flexctc(args):
     value = frames_all * synth.FRAME_SECONDS * args.steps / t_dec
     fbps = frames_all * wl.beam * args.steps / t_dec
 
-    # roofline of the dominant kernel (the persistent beam kernel): algorithmic bytes per launch =
-    # Σ_b L_b · (4·V' [read D once] + 3·K [u8 parent + u16 label backpointers])
-    alg_bytes = frames_local * (4 * Vp1 + 3 * wl.beam)
+    # roofline of the dominant kernel: algorithmic bytes per launch =
+    #  beam kernel:         Σ_b L_b · (4·V' [read D once] + 3·K [u8 parent + u16 label backpointers])
+    #  plain greedy (K=1):  frame_top2_kernel, Σ_b L_b · (4·V' + 16 [{d1, w1, d2} frame summary])
+    #  fused greedy (K=1):  greedy_fused_kernel, Σ_b L_b · 4·V'
+    plain_greedy = wl.beam == 1 and not wl.lm and not wl.boost and wl.beta == 0.0
+    if wl.beam > 1:
+        alg_bytes, kname = frames_local * (4 * Vp1 + 3 * wl.beam), "ctc_beam_kernel (persistent)"
+        note = "latency-bound recurrence: T_max dependent frame steps; see DESIGN.md"
+    elif plain_greedy:
+        alg_bytes, kname = frames_local * (4 * Vp1 + 16), "frame_top2_kernel (HBM stream of D)"
+        note = "fully parallel over frames: bandwidth-bound; see DESIGN.md"
+    else:
+        alg_bytes, kname = frames_local * 4 * Vp1, "greedy_fused_kernel (warp per utterance)"
+        note = "latency-bound recurrence over T frames per utterance; see DESIGN.md"
     kern_s = t_kern / args.steps
     achieved = alg_bytes / kern_s / 1e9
     peak, peak_src = peaks()
-    traffic, traffic_src = ncu_traffic(args.workload)
+    traffic, traffic_src = ncu_traffic(args.workload if not args.beam else f"{args.workload}_k{args.beam}")
 
     # e2e through the public host-buffer entry (flexctc_decode_host): H2D + decode + D2H per step
     e2e = None
@@ -347,10 +364,10 @@ def run_flexctc(args):
             "frames_beams_per_s": fbps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "ctc_beam_kernel (persistent)", "kernel_ms": 1e3 * kern_s,
+                         "kernel": kname, "kernel_ms": 1e3 * kern_s,
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                          "traffic_source": traffic_src,
-                         "note": "latency-bound recurrence: T_max dependent frame steps; see DESIGN.md"},
+                         "note": note},
             "gpu_launches": 2 * args.steps,
             "clocks": clk,
             "e2e": e2e,

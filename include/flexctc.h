@@ -127,11 +127,14 @@ size_t flexctc_workspace_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_
 
 /* ---------------------------------------------------------------------------------------
  * flexctc_decode — Algorithm 1 for a batch, 1-best output (R22).
+ * K = 1 runs the greedy kernels (one bandwidth-bound frame-summary pass
+ * over D, then a warp per utterance; same outputs as Algorithm 1 with a beam of one).
  *   log_probs   device fp32, element (b, t, w) at log_probs[b·stride_b + t·stride_t + w];
  *               unit stride over w; blank id = Vp1-1 (R1). Frames t >= lengths[b] are never
  *               read (R16: NaN padding is allowed).
  *   lengths     device int32 [B]; values outside [0, T] are clamped and flagged.
- *   B, T, Vp1   batch, padded frames, V+1 (2 <= Vp1 <= 8192).
+ *   B, T, Vp1   batch, padded frames, V+1 (2 <= Vp1 <= 8192). With T = 0 the [B, T] arrays
+ *               (log_probs, out_tokens, out_timestamps, out_alignment) may be NULL.
  *   cfg         host pointer; lm / boost may be NULL (fusion term off).
  *   workspace   device buffer of at least flexctc_workspace_bytes(B, T, Vp1, cfg) bytes.
  *   out_tokens      device int32 [B, T]: best transcript, -1 padded.

@@ -89,6 +89,7 @@ WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K) {
     w.bp_parent = o; o += align256((size_t)B * T * K);
     w.bp_label = o; o += align256((size_t)B * T * K * 2);
     w.align_ws = o; o += align256((size_t)B * T * 4);
+    w.greedy = o; o += K == 1 ? align256((size_t)B * T * 16) : 0;  // plain greedy frame summaries
     w.total = o;
     return w;
 }
@@ -277,9 +278,11 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (B == 0) return FLEXCTC_OK;
-    if (!is_device_ptr(log_probs, dev) || !is_device_ptr(lengths, dev) || !is_device_ptr(workspace, dev) ||
-        !is_device_ptr(out_tokens, dev) || !is_device_ptr(out_num_tokens, dev) || !is_device_ptr(out_scores, dev) ||
-        (out_timestamps && !is_device_ptr(out_timestamps, dev)) || (out_alignment && !is_device_ptr(out_alignment, dev)))
+    // T = 0: the [B, T] arrays are empty and may be NULL (nothing is read or written there)
+    auto dev_bt = [&](const void* q, bool required) { return T == 0 ? true : (q ? is_device_ptr(q, dev) : !required); };
+    if (!dev_bt(log_probs, true) || !is_device_ptr(lengths, dev) || !is_device_ptr(workspace, dev) ||
+        !dev_bt(out_tokens, true) || !is_device_ptr(out_num_tokens, dev) || !is_device_ptr(out_scores, dev) ||
+        !dev_bt(out_timestamps, false) || !dev_bt(out_alignment, false))
         return fail(FLEXCTC_ERR_INVALID_ARG, "every buffer must be device memory of the current device (no CPU path)");
     if (lm) {
         if (lm->device != dev || !lm->dmem) return fail(FLEXCTC_ERR_INVALID_ARG, "LM handle belongs to another device");
@@ -309,6 +312,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.bp_parent = (uint8_t*)(w + wl.bp_parent);
     p.bp_label = (uint16_t*)(w + wl.bp_label);
     p.align_ws = (int32_t*)(w + wl.align_ws);
+    p.greedy_sum = cfg->beam == 1 ? (float4*)(w + wl.greedy) : nullptr;
     p.nch = wl.nch;
     p.out_tokens = out_tokens; p.out_num = out_num_tokens; p.out_scores = out_scores;
     p.out_ts = out_timestamps; p.out_align = out_alignment;

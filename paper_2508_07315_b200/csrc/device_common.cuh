@@ -1,0 +1,156 @@
+// Device helpers shared by the beam kernel (beam_kernel.cu) and the greedy kernels
+// (greedy_kernel.cu): orderable score keys, cp.async row staging, the NGPU-LM arc query.
+// Product code only; nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "flexctc_internal.h"
+
+namespace flexctc {
+namespace dev {
+
+constexpr float kNeg = -INFINITY;
+
+__device__ __forceinline__ uint64_t hash_extend(uint64_t h, int w) {  // SPEC S:58 (FNV-64 prime)
+    return (h ^ (uint64_t)(w + 1)) * 1099511628211ull;
+}
+
+__device__ __forceinline__ uint32_t ord_of(float s) {
+    uint32_t u = __float_as_uint(s);
+    if (u == 0x80000000u) u = 0u;  // -0 == +0
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float score_of(uint64_t key) {
+    const uint32_t o = (uint32_t)(key >> 32);
+    const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(u);
+}
+__device__ __forceinline__ uint64_t make_key(float s, uint32_t f) {
+    return ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - f);
+}
+__device__ __forceinline__ uint32_t flat_of(uint64_t key) { return 0xffffffffu - (uint32_t)key; }
+// (slot k, token w) -> an index ordered exactly like the flat index k·V' + w (w < 2^16)
+__device__ __forceinline__ uint32_t flat_idx(int k, int w) { return ((uint32_t)k << 16) | (uint32_t)w; }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// NGPU-LM query from a cached state record: log P(w | state) and the next state.
+// All arc levels (contexts of length >= 2) are binary-searched in lockstep (their loads are
+// independent), the level-1 dense row is loaded in parallel, and the first level holding w
+// wins; cum values are the fp32 backoff sums of the sequential walk (lm_query_host, R19).
+template <int LMV>  // max arc levels (order - 2)
+__device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict__ rec, int w, int& next) {
+    const int n = rec[0], u = rec[1];
+    int2 d = make_int2(0, 0);
+    if (u >= 0) d = __ldg(&lm.dense[(size_t)u * lm.V + w]);
+    int lo[LMV], hi[LMV], hlp[LMV], hnx[LMV];
+    bool hit[LMV];
+#pragma unroll
+    for (int j = 0; j < LMV; ++j) {
+        lo[j] = j < n ? rec[8 + 3 * j] : 0;
+        hi[j] = j < n ? lo[j] + rec[8 + 3 * j + 1] : 0;
+        hit[j] = false;
+        hlp[j] = 0;
+        hnx[j] = 0;
+    }
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < LMV; ++j) {
+            if (lo[j] < hi[j]) {
+                any = true;
+                const int mid = (lo[j] + hi[j]) >> 1;
+                const int4 a = __ldg(&lm.arcs[mid]);  // the whole arc: a hit needs no reload
+                if (a.x == w) { hit[j] = true; hlp[j] = a.y; hnx[j] = a.z; hi[j] = lo[j]; }
+                else if (a.x < w) lo[j] = mid + 1;
+                else hi[j] = mid;
+            }
+        }
+        if (!any) break;
+    }
+#pragma unroll
+    for (int j = 0; j < LMV; ++j) {
+        if (hit[j]) {
+            next = hnx[j];
+            return __fadd_rn(__int_as_float(rec[8 + 3 * j + 2]), __int_as_float(hlp[j]));
+        }
+    }
+    if (u >= 0) {
+        const bool found = (d.y & 0x80000000) != 0;
+        next = d.y & 0x7fffffff;
+        return __fadd_rn(__int_as_float(found ? rec[2] : rec[3]), __int_as_float(d.x));
+    }
+    next = __ldg(&lm.uni_next[w]);
+    return __fadd_rn(__int_as_float(rec[3]), __ldg(&lm.uni_lp[w]));
+}
+
+// A ring slot holds one frame row at float offset row_off(src) (0..3) so that shared and global
+// addresses agree mod 16 B: every row, aligned or not (4100-B rows at V' = 1025), is copied with
+// 16-B cp.async except for <= 3 head and tail elements.
+__device__ __forceinline__ int row_off(const float* src) { return (int)(((uintptr_t)src >> 2) & 3); }
+
+// issued by `nt` threads with local index `tid` (all threads, or the helper warps)
+// overread: the buffer is library-owned (16-B aligned, >= 16 B of slack after the last row), so
+// the row is covered by whole 16-B blocks, the neighbouring rows' bytes landing unused in the slot.
+__device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1, int tid, int nt, int overread) {
+    const int off = row_off(src);
+    if (overread) {
+        const float* g = src - off;
+        const int n16 = (off + Vp1 + 3) >> 2;
+        for (int i = tid; i < n16; i += nt) cp_async16(slot + 4 * i, g + 4 * i);
+        return;
+    }
+    float* dst = slot + off;
+    const int h = min((4 - off) & 3, Vp1);
+    if (tid < h) cp_async4(dst + tid, src + tid);
+    const int n4 = (Vp1 - h) >> 2;
+    for (int i = tid; i < n4; i += nt) cp_async16(dst + h + 4 * i, src + h + 4 * i);
+    const int t0 = h + 4 * n4;
+    if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
+}
+
+// Streamed input (flexctc_decode_host): wait until frame r of every utterance has landed.
+// `ready` caches the last value seen by this thread (frames only ever become ready). A 10 s
+// watchdog flags FLEXCTC_FLAG_STREAM_TIMEOUT instead of hanging the device.
+__device__ __forceinline__ void wait_ready(const DecodeParams& p, int r, int& ready) {
+    if (!p.ready || r < ready) return;
+    const long long t0 = clock64();
+    uint32_t v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready) : "memory");
+        if ((int)v > r) break;
+        if (clock64() - t0 > 20000000000ll) {
+            atomicOr(p.flags, FLEXCTC_FLAG_STREAM_TIMEOUT);
+            v = 0x7fffffffu;
+            break;
+        }
+        __nanosleep(200);
+    }
+    ready = (int)v;
+}
+
+// per-CTA device counters (SURVEY §5 "device counters"), flushed per utterance
+enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEvalDense, kCompactions,
+            kStageA, kDeferredNext,
+            // SM cycles (thread 0) per frame phase: 1-3, 4, LM row builds (inside 4), 5, 6-7;
+            // frames with listed tokens and their cycles
+            kCycP13, kCycP4, kCycRows, kCycP5, kCycP67, kHeavyFrames, kCycHeavy,
+            // finer split: frame top (row issue + wait), phase 2, phase 3, phase 4 setup / collect / evaluate
+            kCycTop, kCycP2, kCycP3, kCycP4Setup, kCycP4Collect, kCycP4Eval, kNumStats };
+
+}  // namespace dev
+}  // namespace flexctc

@@ -108,6 +108,7 @@ struct DecodeParams {
     uint8_t* bp_parent;   // [B][T][K]
     uint16_t* bp_label;   // [B][T][K]
     int32_t* align_ws;    // [B][T]
+    float4* greedy_sum;   // [B][T] {d1, w1, d2, 0} frame summaries of the plain greedy path (K = 1)
     int32_t nch;
     // outputs
     int32_t* out_tokens;
@@ -118,13 +119,14 @@ struct DecodeParams {
 };
 
 struct WorkspaceLayout {
-    size_t flags, order, len_c, chunk_anc, bp_parent, bp_label, align_ws, total;
+    size_t flags, order, len_c, chunk_anc, bp_parent, bp_label, align_ws, greedy, total;
     int32_t nch;
 };
 WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K);
 
-// launches (beam_kernel.cu)
+// launches (beam_kernel.cu; K = 1 goes to launch_greedy in greedy_kernel.cu)
 int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
+int launch_greedy(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
 
 }  // namespace flexctc
 

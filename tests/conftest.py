@@ -20,3 +20,23 @@ def golden():
     import json
     with open(os.path.join(GOLDEN, "values.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def lm_pair():
+    """The synthetic 4-gram LM (c3-c5) as a device handle, an oracle handle, and its path."""
+    import oracle
+    import paper_2508_07315_b200 as F
+    import synth
+    path = synth.arpa_file(V=1024)
+    return F.LM(path, 1024, device=0), oracle.LM(path, 1024), path
+
+
+@pytest.fixture(scope="session")
+def bt_pair():
+    """The 1000 synthetic phrases (c4, c5) as device and oracle boosting handles."""
+    import oracle
+    import paper_2508_07315_b200 as F
+    import synth
+    ph = synth.phrases(1024)
+    return F.Boost(ph, 1.0, 1024, device=0), oracle.Boost(ph, 1.0, 1024), ph

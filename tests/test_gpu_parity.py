@@ -25,18 +25,6 @@ TOL = 1e-4
 NTH = os.cpu_count() or 4
 
 
-@pytest.fixture(scope="session")
-def lm_pair():
-    path = synth.arpa_file(V=1024)
-    return F.LM(path, 1024, device=0), oracle.LM(path, 1024), path
-
-
-@pytest.fixture(scope="session")
-def bt_pair():
-    ph = synth.phrases(1024)
-    return F.Boost(ph, 1.0, 1024, device=0), oracle.Boost(ph, 1.0, 1024), ph
-
-
 def gpu_decode(D, L, cfg, lm=None, bt=None, Vp1=None, alignment=True):
     Dt = torch.from_numpy(np.ascontiguousarray(D)).cuda() if isinstance(D, np.ndarray) else D
     Lt = torch.from_numpy(np.asarray(L, dtype=np.int32)).cuda()

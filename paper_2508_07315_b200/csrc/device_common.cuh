@@ -143,6 +143,53 @@ __device__ __forceinline__ void wait_ready(const DecodeParams& p, int r, int& re
     ready = (int)v;
 }
 
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier ----------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// orders this thread's generic-proxy shared accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    } while (!ok);
+}
+
+// One frame row into a 16-B aligned ring slot at float offset row_off(src) (the layout of
+// load_row), called by all 32 lanes of a warp: lane 0 issues a single bulk copy of the row's
+// covering 16-B blocks when those lie inside [lo, hi) (the tensor's bytes: nothing outside the
+// caller's buffer is read); otherwise (at most the first and the last row of a tensor) the warp
+// copies the row with plain loads and lane 0 arrives without a transaction count.
+// Completion: mbarrier `bar` (count 1).
+__device__ __forceinline__ void bulk_row(float* slot, const float* src, int Vp1, uint64_t* bar, const char* lo,
+                                         const char* hi, int lane) {
+    const int off = row_off(src);
+    const char* g = (const char*)(src - off);
+    const uint32_t bytes = (uint32_t)(((off + Vp1) * 4 + 15) & ~15);
+    if (g >= lo && g + bytes <= hi) {
+        if (lane == 0) {
+            fence_proxy_async();  // earlier generic reads of this slot before the async write
+            mbar_arrive_tx(bar, bytes);
+            bulk_g2s(slot, g, bytes, bar);
+        }
+    } else {
+        for (int w = lane; w < Vp1; w += 32) slot[off + w] = __ldg(src + w);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    }
+}
+
 // per-CTA device counters (SURVEY §5 "device counters"), flushed per utterance
 enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEvalDense, kCompactions,
             kStageA, kDeferredNext,

@@ -18,7 +18,8 @@
 //    runner-up ties after rounding, and collapses the labels to tokens + timestamps (R20).
 //  * fused (β != 0 or LM or boosting): the hypothesis' LM / boost state couples the frames, so
 //    one warp per utterance runs the frame loop (4 utterances per CTA, LPT work queue) after the
-//    same summary pass. Rows stream into a per-warp cp.async ring 7 frames ahead; per frame: the
+//    same summary pass. Rows stream into a per-warp ring 7 frames ahead, one TMA bulk copy
+//    (cp.async.bulk, completion on an mbarrier) per row issued by one lane; per frame: the
 //    summary gives the best non-blank tokens without a scan, exact blank and repeat
 //    candidates, the exact score of the best non-repeat token, then only tokens whose
 //    bound D[w] + ub(state) can reach the running best are scored (LM arc query + boost table
@@ -285,6 +286,12 @@ __global__ void __launch_bounds__(128) greedy_chain_kernel(const DecodeParams p)
 constexpr int kGW = 4;     // utterances (warps) per CTA
 constexpr int kGRing = 8;  // frame rows in flight per warp (covers HBM latency at ~300-cycle frames)
 
+__host__ __device__ __forceinline__ size_t greedy_warp_smem(int Vp1, int RWS) {
+    const int VP = (Vp1 + 3) & ~3;
+    const size_t a = (((size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)Vp1 * 2 + 7) & ~size_t(7));
+    return (a + 8 * kGRing + 15) & ~size_t(15);
+}
+
 __device__ __forceinline__ float4 shfl4(float4 v, int src) {
     return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
                        __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
@@ -299,16 +306,27 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
     const int RWS = lm_on ? ((p.lm.RW + 3) & ~3) : 4;
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
-    // layout: [kGW] x {ring[kGRing][VP + 4] f32, rec[RWS] i32, list[Vp1] u16}, then btroot[V] int2
-    const size_t per_warp = ((size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)Vp1 * 2 + 15) & ~size_t(15);
+    // layout: [kGW] x {ring[kGRing][VP + 4] f32, rec[RWS] i32, list[Vp1] u16, bar[kGRing] u64},
+    // then btroot[V] int2
+    const size_t per_warp = greedy_warp_smem(Vp1, RWS);
     unsigned char* base = smem_raw + (size_t)wid * per_warp;
     float* ring = (float*)base;
     int* rec = (int*)(base + (size_t)kGRing * (VP + 4) * 4);
     uint16_t* list = (uint16_t*)(base + (size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4);
+    uint64_t* bar = (uint64_t*)(base + (((size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)Vp1 * 2 + 7) & ~size_t(7)));
     int2* btroot = (int2*)(smem_raw + (size_t)kGW * per_warp);
     if (bt_on)
         for (int w = threadIdx.x; w < V; w += blockDim.x) btroot[w] = __ldg(&p.bt.tab[w]);
+    if (lane == 0) {
+        for (int i = 0; i < kGRing; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
     __syncthreads();
+    uint32_t ph = 0;  // expected parity of each ring slot's next completion
+    // the tensor's byte range: bulk copies never read outside it (overread: 16 B of slack after)
+    const char* lo = (const char*)p.log_probs;
+    const char* hi = lo + 4 * ((int64_t)(p.B - 1) * p.stride_b + (int64_t)(p.T - 1) * p.stride_t + Vp1) +
+                     (p.overread ? 16 : 0);
     unsigned long long st_frames = 0, st_listed = 0, st_eval = 0;
     int ready = 0;
 
@@ -351,13 +369,13 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
         const float4 none4 = make_float4(kNeg, kNeg, kNeg, __uint_as_float(0xffffffffu));
         float4 sum_c = lane < L ? summ[lane] : none4;
         float4 sum_n = 32 + lane < L ? summ[32 + lane] : none4;
-        for (int r = 0; r < kGRing - 1; ++r) {  // prologue
-            if (r < L) {
-                wait_ready(p, r, ready);
-                load_row(ring + (size_t)r * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, lane, 32, p.overread);
-            }
-            cp_commit();
+        // frame rows: one TMA bulk copy per row (lane 0), kGRing - 1 rows ahead
+        int nissued = 0, ncons = 0;
+        for (int r = 0; r < kGRing - 1 && r < L; ++r) {
+            wait_ready(p, r, ready);
+            bulk_row(ring + (size_t)r * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, &bar[r], lo, hi, lane);
         }
+        nissued = min(kGRing - 1, L);
         for (int t = 0; t < L; ++t) {
             if ((t & 31) == 0 && t) {
                 sum_c = sum_n;
@@ -367,15 +385,19 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
                 const int r = t + kGRing - 1;
                 if (r < L) {
                     wait_ready(p, r, ready);
-                    load_row(ring + (size_t)(r % kGRing) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, lane, 32,
-                             p.overread);
+                    bulk_row(ring + (size_t)(r % kGRing) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1,
+                             &bar[r % kGRing], lo, hi, lane);
+                    nissued = r + 1;
                 }
-                cp_commit();
             }
             const float4 fs4 = shfl4(sum_c, t & 31);
             const int w1 = (int)(__float_as_uint(fs4.w) & 0xffffu);
-            cp_wait<kGRing - 1>();
-            __syncwarp();
+            {
+                const int sl = t % kGRing;
+                mbar_wait(&bar[sl], (ph >> sl) & 1u);
+                ph ^= 1u << sl;
+                ncons = t + 1;
+            }
             const float* row = ring + (size_t)(t % kGRing) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
             // exact blank / repeat candidates: no β, no fusion
             uint64_t best = 0;
@@ -427,7 +449,9 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
                     const float mg = 1e-4f * (1.0f + fabsf(bs) + fabsf(acc) + fabsf(ub));
                     const float dthr = best ? __fsub_rn(__fsub_rn(__fsub_rn(bs, acc), ub), mg) : kNeg;
                     int m = 0;
-                    for (int w0 = 0; w0 < blank; w0 += 32) {
+                    // d2 bounds every non-blank value but w1's: no other token can pass the bound
+                    const bool none_else = wt == w1 && !(fs4.y >= dthr);
+                    for (int w0 = 0; w0 < blank && !none_else; w0 += 32) {
                         const int w = w0 + lane;
                         const float v = w < blank ? row[w] : kNeg;
                         const bool hit = w < blank && w != last && w != wt && v > kNeg && v >= dthr;
@@ -479,7 +503,11 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
             acc = score_of(best);
             last = ws;
         }
-        cp_wait<0>();
+        for (int f = ncons; f < nissued; ++f) {  // rows issued past a dead frame: drain the ring
+            const int sl = f % kGRing;
+            mbar_wait(&bar[sl], (ph >> sl) & 1u);
+            ph ^= 1u << sl;
+        }
         __syncwarp();
         // EOS: + α_LM·LM.Final(state); optional boost retraction (R17)
         float fs = acc;
@@ -499,9 +527,8 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
 
 template <int LMV>
 int launch_fused(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
-    const int VP = (p.Vp1 + 3) & ~3;
     const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
-    const size_t per_warp = ((size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)p.Vp1 * 2 + 15) & ~size_t(15);
+    const size_t per_warp = greedy_warp_smem(p.Vp1, RWS);
     const size_t smem = kGW * per_warp + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0);
     if (smem > 200 * 1024) { err = "shared memory requirement too large (V+1)"; return 2; }
     auto kern = greedy_fused_kernel<LMV>;

@@ -106,9 +106,10 @@ def test_plain_greedy_strides(pad):
 
 def test_greedy_zero_frames(lm_pair):
     """T = 0 (every length 0): empty transcripts, score = α_LM·LM.Final(<s>) (reading of §8(b))."""
-    D = np.zeros((3, 0, 1025), np.float32)
+    D = np.zeros((3, 1, 1025), np.float32)  # the oracle's view: one frame, never read (L = 0)
     for cfg, lm in ((F.config(1), None), (F.config(1, alpha_lm=0.5, beta=0.5), lm_pair)):
         g = gpu_decode(torch.zeros((3, 0, 1025), device="cuda"), [0, 0, 0], cfg, lm[0] if lm else None)
         o = oracle.decode(D, [0, 0, 0], ocfg(cfg), lm[1] if lm else None, None, 1, with_alignment=True)
-        compare(g, o, bitwise=True)
-        assert g["num_tokens"].tolist() == [0, 0, 0]
+        assert g["tokens"].shape == (3, 0)
+        assert g["num_tokens"].tolist() == [0, 0, 0] == o["num_tokens"].tolist()
+        assert np.array_equal(g["scores"].view(np.int32), o["scores"].view(np.int32))

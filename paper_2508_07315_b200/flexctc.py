@@ -61,10 +61,16 @@ STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_f
 
 
 def _load() -> ctypes.CDLL:
+    path = os.environ.get("FLEXCTC_LIB_AB")  # A/B timing of two builds (tools/ab.sh); never a fallback
+    if path:
+        return _declare(ctypes.CDLL(path))
     path = _build.LIB
     if not _build.up_to_date():
         _build.build()  # missing or stale (sources newer); nvcc is part of the image, failures raise
-    L = ctypes.CDLL(path)
+    return _declare(ctypes.CDLL(path))
+
+
+def _declare(L: ctypes.CDLL) -> ctypes.CDLL:
     vp, i32, i64, f32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
     P = ctypes.POINTER
     L.flexctc_last_error.restype = ctypes.c_char_p

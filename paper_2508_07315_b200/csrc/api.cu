@@ -134,6 +134,8 @@ flexctc_status flexctc_lm_load(const char* arpa_path, int32_t vocab_size, const 
         lm->dev.rec = (const int4*)(d + o_rec);
         lm->dev.dense = (const int2*)(d + o_den);
         lm->dev.arcs = (const int4*)(d + o_arc);
+        lm->dev.dense_bytes = (int64_t)h.dense.size() * 4;
+        lm->dev.arcs_bytes = (int64_t)arcs4.size() * 4;
         lm->dev.uni_lp = (const float*)(d + o_ulp);
         lm->dev.uni_next = (const int32_t*)(d + o_unx);
         lm->dev.RW = h.RW;
@@ -201,6 +203,7 @@ flexctc_status flexctc_boost_build(const int32_t* tokens, const int64_t* offsets
         bt->dbytes = up.total();
         char* d = (char*)bt->dmem;
         bt->dev.tab = (const int2*)(d + o_tab);
+        bt->dev.tab_bytes = (int64_t)h.tab.size() * 4;
         bt->dev.U = (const float*)(d + o_u);
         bt->dev.maxd = (const float*)(d + o_m);
         bt->dev.V = h.V;

@@ -46,6 +46,7 @@ struct LmDev {
     const float* uni_lp;
     const int32_t* uni_next;
     int32_t RW, V, start, NL;
+    int64_t dense_bytes, arcs_bytes;  // sizes of dense / arcs (the L2 warm-up ranges)
 };
 constexpr int kMaxLmLevels = 6;    // arc levels (order - 2); order <= 8
 
@@ -64,6 +65,7 @@ struct BoostDev {
     const float* U;
     const float* maxd;
     int32_t V;
+    int64_t tab_bytes;
 };
 
 flexctc_status build_lm_host(const char* path, int32_t V, const char* const* syms, LmHost& out);

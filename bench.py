@@ -309,7 +309,7 @@ def run_flexctc(args):
         alg_bytes, kname = frames_local * (4 * Vp1 + 3 * wl.beam), "ctc_beam_kernel (persistent)"
         note = "latency-bound recurrence: T_max dependent frame steps; see DESIGN.md"
     elif plain_greedy:
-        alg_bytes, kname = frames_local * (4 * Vp1 + 16), "frame_top2_kernel (HBM stream of D)"
+        alg_bytes, kname = frames_local * (4 * Vp1 + 16), "frame_summary_kernel (HBM stream of D)"
         note = "fully parallel over frames: bandwidth-bound; see DESIGN.md"
     else:
         alg_bytes, kname = frames_local * 4 * Vp1, "greedy_fused_kernel (warp per utterance)"
@@ -368,7 +368,10 @@ def run_flexctc(args):
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                          "traffic_source": traffic_src,
                          "note": note},
-            "gpu_launches": 2 * args.steps,
+            # our kernels per decode: order_kernel (not on the plain greedy path), l2_warm_kernel (with
+            # LM or boost), then the beam kernel, or frame_summary_kernel + greedy_chain/fused kernel
+            "gpu_launches": args.steps * ((0 if plain_greedy else 1) + (1 if (wl.lm or wl.boost) else 0)
+                                          + (1 if wl.beam > 1 else 2)),
             "clocks": clk,
             "e2e": e2e,
             "device_flags": flags,

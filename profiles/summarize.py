@@ -56,7 +56,10 @@ def launches(path):
     agg = {}
     for r in rows[1:]:
         name = r[ik]
-        short = "ctc_beam_kernel" if "ctc_beam_kernel" in name else ("order_kernel" if "order_kernel" in name else name[:60])
+        if "flexctc::" in name:  # our kernels: bare name without namespace / template / arguments
+            short = name.replace("<unnamed>::", "").replace("void ", "").split("(")[0].split("<")[0].split("::")[-1]
+        else:
+            short = name[:60]
         t = float(r[iv].replace(",", "")) * (UNIT.get(r[iu], 1e-9) if iu is not None else 1e-9)
         a = agg.setdefault(short, [0, 0.0])
         a[0] += 1
@@ -72,6 +75,9 @@ def main():
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--frames", type=int, default=25600)
     ap.add_argument("--note", default="")
+    ap.add_argument("--kernel", default="ctc_beam_kernel", help="substring of the captured kernel's name")
+    ap.add_argument("--alg-per-frame", type=float, default=4 * 1025 + 3 * 16,
+                    help="algorithmic bytes per utterance-frame (DESIGN.md)")
     a = ap.parse_args()
     md = [f"# ncu summary ({a.tag}, workload {a.workload})", ""]
     if a.note:
@@ -79,9 +85,9 @@ def main():
     js_path = os.path.join(HERE, "ncu_summary.json")
     js = json.load(open(js_path)) if os.path.exists(js_path) else {}
     if a.rep:
-        k = [d for d in raw(a.rep) if "ctc_beam_kernel" in d.get("Kernel Name", ("", ""))[0]]
+        k = [d for d in raw(a.rep) if a.kernel in d.get("Kernel Name", ("", ""))[0]]
         d = k[0]
-        md += ["## `ncu --set full` capture of the beam kernel (one launch, cold L2 after the bench's flush)", "",
+        md += [f"## `ncu --set full` capture of `{a.kernel}` (one launch, cold L2 after the bench's flush)", "",
                "| metric | value | unit |", "|---|---|---|"]
         for m in METRICS:
             if m in d:
@@ -89,7 +95,7 @@ def main():
         rd = to_si(*d["dram__bytes_read.sum"])
         wr = to_si(*d["dram__bytes_write.sum"])
         dur = to_si(*d["gpu__time_duration.sum"])
-        alg = a.frames * (4 * 1025 + 3 * 16)
+        alg = a.frames * a.alg_per_frame
         md += ["", f"DRAM traffic per launch: {(rd + wr) / 1e6:.1f} MB (read {rd / 1e6:.1f} + write {wr / 1e6:.1f}); "
                f"algorithmic bytes {alg / 1e6:.1f} MB; duration under ncu {dur * 1e3:.3f} ms.", ""]
         js[a.workload] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,

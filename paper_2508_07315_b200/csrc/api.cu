@@ -136,6 +136,7 @@ flexctc_status flexctc_lm_load(const char* arpa_path, int32_t vocab_size, const 
         lm->dev.arcs = (const int4*)(d + o_arc);
         lm->dev.dense_bytes = (int64_t)h.dense.size() * 4;
         lm->dev.arcs_bytes = (int64_t)arcs4.size() * 4;
+        lm->dev.rec_bytes = (int64_t)h.rec.size() * 4;
         lm->dev.uni_lp = (const float*)(d + o_ulp);
         lm->dev.uni_next = (const int32_t*)(d + o_unx);
         lm->dev.RW = h.RW;

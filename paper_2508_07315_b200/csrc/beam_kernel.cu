@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             if (tid == 0) st[kCycTop] += (uint32_t)(c0 - ctop);
 
             const int G = solo ? 32 : NT;  // group of the slot-parallel phases
+            long long tp1 = c0, tp2 = c0, tp3 = c0;  // phase boundaries (timers build, thread 0)
             bool stage_a = false;
             int wstar = -1;
             if (bw) {
@@ -544,6 +545,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 // ------------------------------------------------ phase 2: exact candidates of the frame's
                 // best non-blank token (tightens the lower bound of the frame max on emission frames)
                 const long long cp2 = TCLK();
+                tp1 = cp2;
                 float tau0 = __fsub_rn(mxrb, p.theta);
                 if (nalive > 0 && mxrb > kNeg) {
                     const float reach = __fadd_rn(__fadd_rn(accmax, dstar), ubvmax) +
@@ -572,6 +574,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 // ------------------------------------------------ phase 3 (decision): token filter
                 // a non-rb candidate reaching tau0 needs D[w] >= tau0 - accmax - ubvmax (- margin)
                 const long long cp3 = TCLK();
+                tp2 = cp3;
                 if (tid == 0) st[kCycP2] += (uint32_t)(cp3 - cp2);
                 bool scan = false;
                 float dthr = INFINITY;
@@ -602,6 +605,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     st[kStageA] += stage_a ? 1 : 0;
                 }
             }
+            tp3 = TCLK();
             if (solo) __syncthreads();  // B1: the helpers learn whether this frame needs them
             gsync(G);
             const bool scan_all = sc.scan;
@@ -840,6 +844,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 }
             }
             gsync(G);
+            const long long c6 = TCLK();
             // ------------------------------------------------ phase 7: RecombineHypotheses
             unsigned grp = 0;
             const bool small_beam = K <= 32;  // all slots live in warp 0
@@ -851,6 +856,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 const unsigned livemask = __ballot_sync(0xffffffffu, lv);
                 grp = __match_any_sync(0xffffffffu, hk) & __match_any_sync(0xffffffffu, lkey) & livemask;
             }
+            const long long t7a = TCLK();
             int tent = -1;  // K > 32: this slot's entry in the (hash, last) table
             if (NT > 32 && !small_beam) {
                 // groups have <= 3 members (reading R14): a shared hash table keyed on (hash, last)
@@ -871,6 +877,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 }
                 __syncthreads();
             }
+            long long t7b = t7a, t7c = t7a;
             if (tid < K) {
                 const int i = tid;
                 float s = nxt.acc[i];
@@ -932,6 +939,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         if (any && p.merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
                     }
                 }
+                t7b = TCLK();
                 if ((t % kChunk) == kChunk - 1 || t == L - 1)
                     p.chunk_anc[((int64_t)b * p.nch + t / kChunk) * K + i] = nxt.anc[i];
                 // cached records of the new slot states
@@ -952,11 +960,21 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     }
                 }
                 sm.skey[i] = (uint64_t)__float_as_uint(s);  // stash merged score
+                t7c = TCLK();
             }
             gsync(G);
             if (tid < K) nxt.acc[tid] = __uint_as_float((uint32_t)sm.skey[tid]);
             if (tid == 0) {
                 const long long c4 = TCLK();
+                if (m_frame == 0) {  // frames without listed tokens: phase split
+                    st[kLightFrames] += 1;
+                    st[kLP1] += (uint32_t)(tp1 - c0); st[kLP2] += (uint32_t)(tp2 - tp1);
+                    st[kLP3] += (uint32_t)(tp3 - tp2); st[kLB1] += (uint32_t)(c1 - tp3);
+                    st[kLP5] += (uint32_t)(c3 - c2); st[kLP6] += (uint32_t)(c6 - c3);
+                    st[kLP7] += (uint32_t)(c4 - c6);
+                    st[kLP7a] += (uint32_t)(t7a - c6); st[kLP7b] += (uint32_t)(t7b - t7a);
+                    st[kLP7c] += (uint32_t)(t7c - t7b); st[kLP7d] += (uint32_t)(c4 - t7c);
+                }
                 st[kCycP13] += (uint32_t)(c1 - c0); st[kCycP4] += (uint32_t)(c2 - c1);
                 st[kCycP5] += (uint32_t)(c3 - c2); st[kCycP67] += (uint32_t)(c4 - c3);
                 if (m_frame > 0) { st[kHeavyFrames] += 1; st[kCycHeavy] += (uint32_t)(c4 - c0); }
@@ -1081,11 +1099,14 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
 // sorted arcs, the boost transition table): one streaming pass (prefetch.global.L2::evict_last
 // per 128-B line) at HBM rate before the frame loop, so the dependent lookups of the recurrence
 // hit L2 instead of paying HBM latency after every cold start (the bench flushes L2 per step).
-__global__ void l2_warm_kernel(const char* a, int64_t na, const char* b, int64_t nb, const char* c, int64_t nc) {
-    const int64_t la = (na + 127) >> 7, lb = (nb + 127) >> 7, lc = (nc + 127) >> 7;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < la + lb + lc;
+__global__ void l2_warm_kernel(const char* a, int64_t na, const char* b, int64_t nb, const char* c, int64_t nc,
+                               const char* d, int64_t nd) {
+    const int64_t la = (na + 127) >> 7, lb = (nb + 127) >> 7, lc = (nc + 127) >> 7, ld = (nd + 127) >> 7;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < la + lb + lc + ld;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const char* q = i < la ? a + (i << 7) : i < la + lb ? b + ((i - la) << 7) : c + ((i - la - lb) << 7);
+        const char* q = i < la ? a + (i << 7)
+                        : i < la + lb ? b + ((i - la) << 7)
+                        : i < la + lb + lc ? c + ((i - la - lb) << 7) : d + ((i - la - lb - lc) << 7);
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(q));
     }
 }
@@ -1254,9 +1275,12 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
         int dev = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char* e_wr = getenv("FLEXCTC_L2_WARM_REC");  // "1": also the LM state records (A/B)
+        const bool warm_rec = e_wr && e_wr[0] == '1';
         l2_warm_kernel<<<4 * nsm, 256, 0, st>>>((const char*)p.lm.dense, p.use_lm ? p.lm.dense_bytes : 0,
                                                 (const char*)p.lm.arcs, p.use_lm ? p.lm.arcs_bytes : 0,
-                                                (const char*)p.bt.tab, p.use_bt ? p.bt.tab_bytes : 0);
+                                                (const char*)p.bt.tab, p.use_bt ? p.bt.tab_bytes : 0,
+                                                (const char*)p.lm.rec, p.use_lm && warm_rec ? p.lm.rec_bytes : 0);
         e = cudaGetLastError();
         if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     }

@@ -44,6 +44,16 @@ __device__ __forceinline__ void cp_async16(void* s, const void* g) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
 }
+// 16-B copy with an L2 evict-first policy (streamed data that must not displace L2-resident tables)
+__device__ __forceinline__ void cp_async16_ef(void* s, const void* g, uint64_t pol) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "l"(pol));
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -108,17 +118,18 @@ __device__ __forceinline__ int row_off(const float* src) { return (int)(((uintpt
 // the row is covered by whole 16-B blocks, the neighbouring rows' bytes landing unused in the slot.
 __device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1, int tid, int nt, int overread) {
     const int off = row_off(src);
+    const uint64_t pol = policy_evict_first();  // D is read once: keep the LM / boost tables in L2
     if (overread) {
         const float* g = src - off;
         const int n16 = (off + Vp1 + 3) >> 2;
-        for (int i = tid; i < n16; i += nt) cp_async16(slot + 4 * i, g + 4 * i);
+        for (int i = tid; i < n16; i += nt) cp_async16_ef(slot + 4 * i, g + 4 * i, pol);
         return;
     }
     float* dst = slot + off;
     const int h = min((4 - off) & 3, Vp1);
     if (tid < h) cp_async4(dst + tid, src + tid);
     const int n4 = (Vp1 - h) >> 2;
-    for (int i = tid; i < n4; i += nt) cp_async16(dst + h + 4 * i, src + h + 4 * i);
+    for (int i = tid; i < n4; i += nt) cp_async16_ef(dst + h + 4 * i, src + h + 4 * i, pol);
     const int t0 = h + 4 * n4;
     if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
 }
@@ -197,7 +208,12 @@ enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEv
             // frames with listed tokens and their cycles
             kCycP13, kCycP4, kCycRows, kCycP5, kCycP67, kHeavyFrames, kCycHeavy,
             // finer split: frame top (row issue + wait), phase 2, phase 3, phase 4 setup / collect / evaluate
-            kCycTop, kCycP2, kCycP3, kCycP4Setup, kCycP4Collect, kCycP4Eval, kNumStats };
+            kCycTop, kCycP2, kCycP3, kCycP4Setup, kCycP4Collect, kCycP4Eval,
+            // frames without listed tokens: count and cycles of phase 1, 2, 3, B1 (+ phase-4 entry),
+            // 5, 6, 7
+            kLightFrames, kLP1, kLP2, kLP3, kLB1, kLP5, kLP6, kLP7,
+            // phase 7 of those frames: match.any, merge scores, chunk ancestors + records, final sync
+            kLP7a, kLP7b, kLP7c, kLP7d, kNumStats };
 
 }  // namespace dev
 }  // namespace flexctc

@@ -46,7 +46,7 @@ struct LmDev {
     const float* uni_lp;
     const int32_t* uni_next;
     int32_t RW, V, start, NL;
-    int64_t dense_bytes, arcs_bytes;  // sizes of dense / arcs (the L2 warm-up ranges)
+    int64_t dense_bytes, arcs_bytes, rec_bytes;  // sizes (the L2 warm-up ranges)
 };
 constexpr int kMaxLmLevels = 6;    // arc levels (order - 2); order <= 8
 
@@ -81,7 +81,7 @@ float lm_query_host(const LmHost& lm, int32_t s, int32_t w, int32_t* next);
 constexpr int kChunk = 32;      // frames per backtrace chunk (chunk ancestors, §7.3 item 6)
 constexpr int kMaxBeam = 256;   // parent index fits a u8
 constexpr int kMaxVp1 = 8192;   // frame rows are staged in shared memory
-constexpr int kStatsWords = 32; // u64 device counters at workspace + 64 B
+constexpr int kStatsWords = 48; // u64 device counters at workspace + 64 B
 
 struct DecodeParams {
     const float* log_probs;

@@ -39,9 +39,12 @@ def main():
     fr = max(1, s["frames"])
     per = {k: round(v / fr, 1) for k, v in s.items() if k.startswith("cyc_")}
     hv = max(1, s["heavy_frames"])
+    lf = max(1, s.get("light_frames", 0))
+    light = {k: round(v / lf, 1) for k, v in s.items() if k.startswith("lcyc_")}
     out = {"workload": a.workload, "K": K, "counters": s, "cycles_per_frame": per,
            "heavy_fraction": round(s["heavy_frames"] / fr, 3),
-           "cycles_per_heavy_frame": round(s["cyc_heavy_frames"] / hv, 1)}
+           "cycles_per_heavy_frame": round(s["cyc_heavy_frames"] / hv, 1),
+           "light_frame_split": light}
     print(json.dumps(out))
 
 

@@ -153,6 +153,26 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
                               int32_t* out_tokens, int32_t* out_num_tokens, float* out_scores,
                               int32_t* out_timestamps, int32_t* out_alignment);
 
+/* ---------------------------------------------------------------------------------------
+ * flexctc_decode_nbest — flexctc_decode returning the `nbest` best final hypotheses per
+ * utterance instead of one (SPEC --nbest S:494; the final merge R15 ranks
+ * the merged hypotheses by (score desc, slot asc), rank 0 is flexctc_decode's output).
+ *   nbest           1 <= nbest <= cfg->beam (else FLEXCTC_ERR_INVALID_ARG).
+ *   out_tokens      device int32 [B, nbest, T], -1 padded; rows past the number of surviving
+ *                   hypotheses are empty.
+ *   out_num_tokens  device int32 [B, nbest] (0 for empty rows).
+ *   out_scores      device fp32 [B, nbest] (-inf for empty rows).
+ *   out_timestamps  device int32 [B, nbest, T] or NULL.
+ * Everything else (arguments, workspace, errors, asynchrony) as flexctc_decode.
+ * ------------------------------------------------------------------------------------- */
+flexctc_status flexctc_decode_nbest(const float* log_probs, int64_t stride_b, int64_t stride_t,
+                                    const int32_t* lengths, int32_t B, int32_t T, int32_t Vp1,
+                                    const flexctc_config* cfg, const flexctc_lm* lm,
+                                    const flexctc_boost* boost, void* workspace,
+                                    size_t workspace_bytes, flexctc_stream stream, int32_t nbest,
+                                    int32_t* out_tokens, int32_t* out_num_tokens, float* out_scores,
+                                    int32_t* out_timestamps);
+
 /* Measurement hook: when both are non-NULL, subsequent flexctc_decode calls on this thread
  * record `ev_start` (a cudaEvent_t) immediately before and `ev_stop` immediately after the
  * persistent beam kernel on the decode stream, so callers can time that kernel alone.

@@ -267,9 +267,10 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
                                   const flexctc_boost* boost, void* workspace, size_t workspace_bytes,
                                   flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
                                   float* out_scores, int32_t* out_timestamps, int32_t* out_alignment,
-                                  const uint32_t* ready, int overread) {
+                                  const uint32_t* ready, int overread, int32_t nbest = 1) {
     flexctc_status st = validate_cfg(cfg);
     if (st != FLEXCTC_OK) return st;
+    if (nbest < 1 || nbest > cfg->beam) return fail(FLEXCTC_ERR_INVALID_ARG, "nbest must be in [1, beam]");
     if (B < 0 || T < 0) return fail(FLEXCTC_ERR_INVALID_ARG, "B and T must be >= 0");
     if (Vp1 < 2) return fail(FLEXCTC_ERR_INVALID_ARG, "Vp1 must be >= 2");
     if (Vp1 > kMaxVp1) return fail(FLEXCTC_ERR_CAPACITY, "Vp1 > 8192");
@@ -322,6 +323,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.out_ts = out_timestamps; p.out_align = out_alignment;
     p.ready = ready;
     p.overread = overread;
+    p.nbest = nbest;
     std::string err;
     int rc = launch_decode(p, (void*)stream, g_ev_start, g_ev_stop, err);
     if (rc == 2) return fail(FLEXCTC_ERR_CAPACITY, err);
@@ -336,6 +338,16 @@ flexctc_status flexctc_decode(const float* log_probs, int64_t stride_b, int64_t 
                               float* out_scores, int32_t* out_timestamps, int32_t* out_alignment) {
     return decode_impl(log_probs, stride_b, stride_t, lengths, B, T, Vp1, cfg, lm, boost, workspace, workspace_bytes,
                        stream, out_tokens, out_num_tokens, out_scores, out_timestamps, out_alignment, nullptr, 0);
+}
+
+flexctc_status flexctc_decode_nbest(const float* log_probs, int64_t stride_b, int64_t stride_t,
+                                    const int32_t* lengths, int32_t B, int32_t T, int32_t Vp1,
+                                    const flexctc_config* cfg, const flexctc_lm* lm, const flexctc_boost* boost,
+                                    void* workspace, size_t workspace_bytes, flexctc_stream stream, int32_t nbest,
+                                    int32_t* out_tokens, int32_t* out_num_tokens, float* out_scores,
+                                    int32_t* out_timestamps) {
+    return decode_impl(log_probs, stride_b, stride_t, lengths, B, T, Vp1, cfg, lm, boost, workspace, workspace_bytes,
+                       stream, out_tokens, out_num_tokens, out_scores, out_timestamps, nullptr, nullptr, 0, nbest);
 }
 
 void flexctc_set_profile_events(void* ev_start, void* ev_stop) {

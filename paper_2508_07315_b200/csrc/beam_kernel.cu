@@ -996,7 +996,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             sm.skey[tid] = (uint64_t)__float_as_uint(fs);
         }
         __syncthreads();
-        uint64_t bestkey = 0;
+        uint64_t mykey = 0;  // final-merge survivor key: (merged score, ~slot); 0 = not a survivor
         if (tid < K && fs > kNeg) {
             const int i = tid;
             float s = fs;
@@ -1028,66 +1028,83 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     prev_j = bj;
                 }
                 if (any && p.merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
-                bestkey = ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - (uint32_t)i);
+                mykey = ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - (uint32_t)i);
             }
         }
-        bestkey = block_max_u64(bestkey, sc, NT);
-        const bool has_best = bestkey != 0ull;
-        const int best = has_best ? (int)(0xffffffffu - (uint32_t)bestkey) : -1;
-        const float best_score = has_best ? score_of(bestkey) : kNeg;
+        // rank the survivors by (score desc, slot asc): rank r -> slot, merged score
+        const int NB = p.nbest > 1 ? p.nbest : 1;
+        __syncthreads();
+        if (tid < K) sm.ckey[tid] = mykey;
+        int nsurv;
+        block_exscan(mykey ? 1 : 0, &nsurv, sc, NT);
+        __syncthreads();
+        if (mykey) {
+            int rank = 0;
+            for (int j = 0; j < K; ++j) rank += sm.ckey[j] > mykey ? 1 : 0;
+            if (rank < NB) { sm.alive_idx[rank] = tid; sm.slm[rank] = __float_as_int(score_of(mykey)); }
+        }
+        __syncthreads();
 
-        // ------------------------------------------------------------ backtrace ("reconstruction on demand")
-        int32_t* align = (p.out_align ? p.out_align : p.align_ws) + (int64_t)b * p.T;
-        const int nchk = (L + kChunk - 1) / kChunk;
-        if (has_best && L > 0) {
-            if (tid == 0) {
-                int s = best;
-                sm.endslot[nchk - 1] = s;
-                for (int c = nchk - 1; c >= 1; --c) {
-                    s = p.chunk_anc[((int64_t)b * p.nch + c) * K + s];
-                    sm.endslot[c - 1] = s;
+        for (int r = 0; r < NB; ++r) {  // the 1-best (NB = 1) or the n best merged hypotheses
+            const bool has_best = r < nsurv;
+            const int best = has_best ? sm.alive_idx[r] : -1;
+            const float best_score = has_best ? __int_as_float(sm.slm[r]) : kNeg;
+            const int64_t orow = (int64_t)b * NB + r;  // output row
+            // ------------------------------------------------------------ backtrace ("reconstruction on demand")
+            int32_t* align = (p.out_align && r == 0 ? p.out_align : p.align_ws) + (int64_t)b * p.T;
+            const int nchk = (L + kChunk - 1) / kChunk;
+            if (has_best && L > 0) {
+                if (tid == 0) {
+                    int s = best;
+                    sm.endslot[nchk - 1] = s;
+                    for (int c = nchk - 1; c >= 1; --c) {
+                        s = p.chunk_anc[((int64_t)b * p.nch + c) * K + s];
+                        sm.endslot[c - 1] = s;
+                    }
+                }
+                __syncthreads();
+                for (int c = tid; c < nchk; c += NT) {
+                    int s = sm.endslot[c];
+                    const int t_hi = min(c * kChunk + kChunk - 1, L - 1);
+                    for (int t = t_hi; t >= c * kChunk; --t) {
+                        const int64_t o = ((int64_t)b * p.T + t) * K + s;
+                        align[t] = p.bp_label[o];
+                        s = p.bp_parent[o];
+                    }
                 }
             }
             __syncthreads();
-            for (int c = tid; c < nchk; c += NT) {
-                int s = sm.endslot[c];
-                const int t_hi = min(c * kChunk + kChunk - 1, L - 1);
-                for (int t = t_hi; t >= c * kChunk; --t) {
-                    const int64_t o = ((int64_t)b * p.T + t) * K + s;
-                    align[t] = p.bp_label[o];
-                    s = p.bp_parent[o];
+            // collapse to tokens + timestamps (R20): emitted at t iff a_t != blank and a_t != a_{t-1}
+            const int per = (L + NT - 1) / NT;
+            const int t0 = min(L, tid * per), t1 = min(L, t0 + per);
+            int cnt = 0;
+            if (has_best)
+                for (int t = t0; t < t1; ++t) {
+                    const int at = align[t], ap = t ? align[t - 1] : blank;
+                    cnt += (at != blank && at != ap) ? 1 : 0;
                 }
-            }
-        }
-        __syncthreads();
-        // collapse to tokens + timestamps (R20): emitted at t iff a_t != blank and a_t != a_{t-1}
-        const int per = (L + NT - 1) / NT;
-        const int t0 = min(L, tid * per), t1 = min(L, t0 + per);
-        int cnt = 0;
-        if (has_best)
-            for (int t = t0; t < t1; ++t) {
-                const int at = align[t], ap = t ? align[t - 1] : blank;
-                cnt += (at != blank && at != ap) ? 1 : 0;
-            }
-        int ntok;
-        int off = block_exscan(cnt, &ntok, sc, NT);
-        int32_t* otok = p.out_tokens + (int64_t)b * p.T;
-        int32_t* ots = p.out_ts ? p.out_ts + (int64_t)b * p.T : nullptr;
-        if (has_best)
-            for (int t = t0; t < t1; ++t) {
-                const int at = align[t], ap = t ? align[t - 1] : blank;
-                if (at != blank && at != ap) {
-                    otok[off] = at;
-                    if (ots) ots[off] = t;
-                    ++off;
+            int ntok;
+            int off = block_exscan(cnt, &ntok, sc, NT);
+            int32_t* otok = p.out_tokens + orow * p.T;
+            int32_t* ots = p.out_ts ? p.out_ts + orow * p.T : nullptr;
+            if (has_best)
+                for (int t = t0; t < t1; ++t) {
+                    const int at = align[t], ap = t ? align[t - 1] : blank;
+                    if (at != blank && at != ap) {
+                        otok[off] = at;
+                        if (ots) ots[off] = t;
+                        ++off;
+                    }
                 }
+            if (!has_best) ntok = 0;
+            for (int i = ntok + tid; i < p.T; i += NT) { otok[i] = -1; if (ots) ots[i] = -1; }
+            if (p.out_align && r == 0)
+                for (int i = (has_best ? L : 0) + tid; i < p.T; i += NT) p.out_align[(int64_t)b * p.T + i] = -1;
+            if (tid == 0) {
+                p.out_num[orow] = ntok;
+                p.out_scores[orow] = best_score;
             }
-        for (int i = ntok + tid; i < p.T; i += NT) { otok[i] = -1; if (ots) ots[i] = -1; }
-        if (p.out_align)
-            for (int i = (has_best ? L : 0) + tid; i < p.T; i += NT) p.out_align[(int64_t)b * p.T + i] = -1;
-        if (tid == 0) {
-            p.out_num[b] = ntok;
-            p.out_scores[b] = best_score;
+            __syncthreads();
         }
     }
 #pragma unroll

@@ -118,6 +118,7 @@ struct DecodeParams {
     float* out_scores;
     int32_t* out_ts;
     int32_t* out_align;   // may alias align_ws
+    int32_t nbest;        // 0 / 1: 1-best; N > 1: out_tokens [B][N][T], out_num / out_scores [B][N]
 };
 
 struct WorkspaceLayout {

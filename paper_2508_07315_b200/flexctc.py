@@ -51,7 +51,7 @@ EXPORTS = [
     "flexctc_last_error", "flexctc_version", "flexctc_lm_load", "flexctc_lm_free", "flexctc_lm_get_info",
     "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
     "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
-    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_set_profile_events", "flexctc_get_stats",
+    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_decode_nbest", "flexctc_set_profile_events", "flexctc_get_stats",
 ]
 STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
               "exact_dense", "compactions", "top_token_stages", "deferred_next",
@@ -90,6 +90,8 @@ def _declare(L: ctypes.CDLL) -> ctypes.CDLL:
     L.flexctc_workspace_bytes.restype = sz
     L.flexctc_decode.argtypes = [vp, i64, i64, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp,
                                  vp, vp, vp, vp, vp]
+    L.flexctc_decode_nbest.argtypes = [vp, i64, i64, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, i32,
+                                       vp, vp, vp, vp]
     L.flexctc_check.argtypes = [vp, P(ctypes.c_uint32)]
     L.flexctc_host_scratch_bytes.argtypes = [i32, i32, i32, P(Config)]
     L.flexctc_host_scratch_bytes.restype = sz
@@ -240,6 +242,36 @@ def decode(log_probs, lengths, cfg: Config, lm: LM | None = None, boost: Boost |
                                   _ptr(outputs["tokens"]), _ptr(outputs["num_tokens"]), _ptr(outputs["scores"]),
                                   _ptr(outputs.get("timestamps")), _ptr(outputs.get("alignment"))))
     return outputs
+
+
+def decode_nbest(log_probs, lengths, cfg: Config, nbest: int, lm: LM | None = None, boost: Boost | None = None,
+                 Vp1: int | None = None, workspace: Workspace | None = None, stream=None):
+    """Enqueue flexctc_decode_nbest: the `nbest` best final hypotheses per utterance, ranked by
+    (score desc, slot asc). Returns CUDA tensors tokens [B, N, T], num_tokens [B, N], scores [B, N],
+    timestamps [B, N, T]; rows past the surviving hypotheses are empty (0 tokens, -inf)."""
+    import torch
+    if not (log_probs.is_cuda and lengths.is_cuda):
+        raise FlexCTCError(1, "decode needs CUDA tensors (there is no CPU path)")
+    if log_probs.dtype != torch.float32 or log_probs.dim() != 3 or log_probs.stride(2) != 1:
+        raise FlexCTCError(1, "log_probs must be float32 [B, T, V'] with unit stride on V'")
+    B, T, W = log_probs.shape
+    Vp1 = W if Vp1 is None else Vp1
+    dev = log_probs.device
+    if workspace is None:
+        workspace = make_workspace(B, T, Vp1, cfg, dev)
+    out = {"tokens": torch.empty((B, nbest, T), dtype=torch.int32, device=dev),
+           "num_tokens": torch.empty((B, nbest), dtype=torch.int32, device=dev),
+           "scores": torch.empty((B, nbest), dtype=torch.float32, device=dev),
+           "timestamps": torch.empty((B, nbest, T), dtype=torch.int32, device=dev)}
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        _check(lib.flexctc_decode_nbest(_ptr(log_probs), log_probs.stride(0), log_probs.stride(1), _ptr(lengths), B,
+                                        T, Vp1, ctypes.byref(cfg), lm.h if lm else None, boost.h if boost else None,
+                                        _ptr(workspace.buf), workspace.nbytes, ctypes.c_void_p(stream.cuda_stream),
+                                        int(nbest), _ptr(out["tokens"]), _ptr(out["num_tokens"]), _ptr(out["scores"]),
+                                        _ptr(out["timestamps"])))
+    return out
 
 
 def set_profile_events(start=None, stop=None):

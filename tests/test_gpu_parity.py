@@ -362,3 +362,45 @@ def test_eq1_replay_max_mode_c5(lm_pair, bt_pair):
         s = _fmaf(f32(cfg.alpha_lm), f32(olm.logp(prefix, -1, f32=True)), s)
         assert prefix == list(g["tokens"][b, :g["num_tokens"][b]])
         assert f32(g["scores"][b]) == s, (b, g["scores"][b], s)
+
+
+@pytest.mark.parametrize("wname,nbest,mode", [("c1", 4, 0), ("c2", 3, 1), ("c3", 16, 0), ("c4", 5, 0), ("c4", 16, 1)])
+def test_nbest_vs_oracle(lm_pair, bt_pair, wname, nbest, mode):
+    """flexctc_decode_nbest (SPEC --nbest): every utterance's ranked final
+    hypotheses (R15 merge, (score desc, slot asc)) equal the oracle's, row 0 equals flexctc_decode."""
+    wl, D, L, _, _ = synth.workload_inputs(wname, B=6 if wname != "c1" else None)
+    cfg = wl_cfg(wl, merge_mode=mode)
+    glm = lm_pair[0] if wl.lm else None
+    gbt = bt_pair[0] if wl.boost else None
+    Dt, Lt = torch.from_numpy(np.ascontiguousarray(D)).cuda(), torch.from_numpy(L.astype(np.int32)).cuda()
+    g = F.decode_nbest(Dt, Lt, cfg, nbest, glm, gbt)
+    one = F.decode(Dt, Lt, cfg, glm, gbt)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in g.items()}
+    one = {k: v.cpu().numpy() for k, v in one.items()}
+    assert np.array_equal(g["tokens"][:, 0], one["tokens"]) and np.array_equal(g["num_tokens"][:, 0], one["num_tokens"])
+    assert np.array_equal(g["timestamps"][:, 0], one["timestamps"])
+    assert np.array_equal(g["scores"][:, 0].view(np.int32), one["scores"].view(np.int32))
+    for b in range(D.shape[0]):
+        ref = oracle.decode_nbest(D[b].astype(np.float64), ocfg(cfg), lm_pair[1] if wl.lm else None,
+                                  bt_pair[1] if wl.boost else None, L=int(L[b]), f32=True)
+        for r in range(nbest):
+            n = int(g["num_tokens"][b, r])
+            if r < len(ref):
+                toks, sc = ref[r]
+                assert tuple(g["tokens"][b, r, :n]) == toks, (b, r)
+                assert (g["tokens"][b, r, n:] == -1).all()
+                if mode == 1:
+                    assert np.float32(g["scores"][b, r]) == np.float32(sc), (b, r)
+                assert abs(float(g["scores"][b, r]) - sc) <= TOL, (b, r, float(g["scores"][b, r]), sc)
+            else:
+                assert n == 0 and g["scores"][b, r] == -np.inf
+
+
+def test_nbest_rejects_bad_n():
+    Dt = torch.zeros((1, 4, 5), device="cuda")
+    Lt = torch.full((1,), 4, dtype=torch.int32, device="cuda")
+    with pytest.raises(F.FlexCTCError):
+        F.decode_nbest(Dt, Lt, F.config(4), 5)
+    with pytest.raises(F.FlexCTCError):
+        F.decode_nbest(Dt, Lt, F.config(4), 0)

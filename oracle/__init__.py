@@ -12,6 +12,8 @@ Parity status per function (details in DESIGN.md "Oracle pins"):
   decode K=1 .......................................... pinned: greedy decoding
   lm_logp / lm_seq .................................... pinned: hand-computed ARPA fixtures
   boost_delta / boost_U ............................... pinned: SPEC S:259-285 hand values, telescoping
+  log_softmax_bf16 (input side, reading R25) .......... pinned: numpy fp64 log-softmax, hand cases,
+        normalisation
   decode at K < #prefixes, θ < ∞ (the beam heuristic) . follows Alg. 1 step by step; the
         truncation itself has no closed form ("parity unpinned" beyond the pins above)
 """
@@ -80,6 +82,8 @@ def lib():
                                         vp, vp, vp, vp, vp]
         L.oracle_decode_nbest.restype = i32
         L.oracle_decode_nbest.argtypes = [vp, i32, i32, i32, P(Cfg), vp, vp, i32, i32, vp, vp, vp]
+        L.oracle_log_softmax_bf16.restype = i32
+        L.oracle_log_softmax_bf16.argtypes = [vp, i64, i64, i32, vp]
     return _lib
 
 
@@ -207,3 +211,16 @@ def decode_nbest(D: np.ndarray, cfg: Cfg, lm: LM | None = None, boost: Boost | N
     if n < 0:
         raise ValueError(_err())
     return [(tuple(int(x) for x in tok[i, :lens[i]]), float(sc[i])) for i in range(min(n, cap))]
+
+
+def log_softmax_bf16(x_bits: np.ndarray) -> np.ndarray:
+    """Log-softmax over the last axis of bf16 logits given as uint16 bit patterns [..., Vp1]
+    (reading R25): fp32 result of (x - lse) with lse = m + log(sum exp(x - m)) in fp64."""
+    x = np.ascontiguousarray(x_bits, dtype=np.uint16)
+    Vp1 = x.shape[-1]
+    rows = x.reshape(-1, Vp1)
+    out = np.empty(rows.shape, np.float32)
+    rc = lib().oracle_log_softmax_bf16(_ptr(rows), rows.shape[0], Vp1, Vp1, _ptr(out))
+    if rc != 0:
+        raise ValueError(_err())
+    return out.reshape(x.shape)

@@ -551,4 +551,25 @@ int32_t oracle_decode_nbest(const double* log_probs, int32_t T, int32_t Vp1, int
     return emit(decode_utt<double>(D, Vp1, L, cfg, (const Arpa*)lm, (const Boost*)bt));
 }
 
+// log-softmax of bf16 logits, the plain definition (R25): bf16 -> its exact value (the upper 16
+// bits of an fp32), max, fp64 sum of exp in index order, lse, one rounding per output
+int32_t oracle_log_softmax_bf16(const uint16_t* x, int64_t n_rows, int64_t stride, int32_t Vp1, float* out) {
+    for (int64_t i = 0; i < n_rows; ++i) {
+        std::vector<double> v(Vp1);
+        for (int w = 0; w < Vp1; ++w) {
+            uint32_t bits = (uint32_t)x[i * stride + w] << 16;
+            float f;
+            std::memcpy(&f, &bits, 4);
+            v[w] = (double)f;
+        }
+        double m = v[0];
+        for (int w = 1; w < Vp1; ++w) m = std::max(m, v[w]);
+        double S = 0.0;
+        for (int w = 0; w < Vp1; ++w) S += std::exp(v[w] - m);
+        const double lse = m + std::log(S);
+        for (int w = 0; w < Vp1; ++w) out[i * Vp1 + w] = (float)(v[w] - lse);
+    }
+    return 0;
+}
+
 }  // extern "C"

@@ -68,6 +68,12 @@ int32_t oracle_decode_nbest(const double* log_probs, int32_t T, int32_t Vp1, int
                             int32_t max_out, int32_t* tokens_out, int32_t* lens_out,
                             double* scores_out);
 
+/* ---- input side (reading R25): log-softmax of bf16 logits ----
+ * Row i of n_rows holds Vp1 bf16 logits at x + i*stride (elements). With the logits as exact
+ * reals: m = max_w x_w; S = sum_w exp(x_w - m) in fp64, index order; lse = m + log(S) (fp64);
+ * out[i*Vp1 + w] = (float)(x_w - lse), the fp64 difference rounded once. Returns 0. */
+int32_t oracle_log_softmax_bf16(const uint16_t* x, int64_t n_rows, int64_t stride, int32_t Vp1, float* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -271,3 +271,48 @@ def test_synthetic_arpa_normalised():
     for h in hists:
         tot = sum(math.exp(lm.logp(h, w)) for w in range(1024)) + math.exp(lm.logp(h, -1))
         assert tot == pytest.approx(1.0, abs=1e-3), h
+
+
+# ----------------------------------------------------------------- input side: bf16 log-softmax
+# SURVEY §8(f) NEXT 4 (log-softmax of bf16 logits fused into the frame read); DESIGN.md reading
+# R25 fixes the arithmetic: exact bf16 values, fp64 max / sum / log, one rounding to fp32.
+
+def _bf16_bits(x):
+    """Round-to-nearest-even fp32 -> bf16 bit patterns (uint16)."""
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return u.astype(np.uint16)
+
+
+def _bf16_value(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def test_log_softmax_bf16_hand_cases():
+    # logits exactly representable in bf16: [0, 1, -2, 0.5]; lse = ln(1 + e + e^-2 + e^0.5)
+    bits = _bf16_bits(np.array([[0.0, 1.0, -2.0, 0.5]], np.float32))
+    out = oracle.log_softmax_bf16(bits)
+    lse = math.log(1 + math.e + math.exp(-2.0) + math.exp(0.5))
+    assert out.tolist() == [[float(np.float32(v - lse)) for v in (0.0, 1.0, -2.0, 0.5)]]
+    # uniform logits: every output is -ln(V') rounded once, whatever the common value
+    for c in (0.0, 7.5, -13.25):
+        bits = _bf16_bits(np.full((2, 1025), c, np.float32))
+        out = oracle.log_softmax_bf16(bits)
+        assert (out == np.float32(-math.log(1025))).all()
+
+
+def test_log_softmax_bf16_matches_numpy_fp64():
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((64, 1025)) * 3.0).astype(np.float32)
+    x[:, 17] += 15.0  # a peaky column, as the synthetic CTC rows
+    bits = _bf16_bits(x)
+    v = _bf16_value(bits)
+    m = v.max(-1, keepdims=True)
+    ref = (v - (m + np.log(np.exp(v - m).sum(-1, keepdims=True)))).astype(np.float32)
+    out = oracle.log_softmax_bf16(bits)
+    # the fp64 sums differ only in summation order (~1e-16 relative): the rounded fp32 outputs
+    # agree exactly except at a rounding boundary, and never by more than one ulp
+    ulp = np.spacing(np.abs(ref))
+    assert (np.abs(out.astype(np.float64) - ref) <= ulp).all()
+    assert (out == ref).mean() > 0.9999
+    assert np.allclose(np.exp(out.astype(np.float64)).sum(-1), 1.0, atol=1e-5)

@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--workload", default="c4", choices=sorted(synth.WORKLOADS))
     ap.add_argument("--impl", default="flexctc", choices=["flexctc", "reference"])
     ap.add_argument("--batch", type=int, default=0, help="override the workload's batch per GPU")
+    ap.add_argument("--input", default="f32-logprobs", choices=["f32-logprobs", "bf16-logits"],
+                    help="bf16-logits: flexctc_decode_logits_bf16, log-softmax fused into the frame read (NEXT 4)")
     ap.add_argument("--beam", type=int, default=0,
                     help="override the workload's beam (1 = the greedy kernels, SURVEY §8(f) NEXT 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -242,8 +244,12 @@ def run_flexctc(args):
     cfg = F.config(wl.beam, wl.alpha_lm if wl.lm else 0.0, wl.alpha_bt if wl.boost else 0.0, wl.beta, wl.theta,
                    wl.merge_mode)
     Dd = torch.from_numpy(D).to(dev)
+    bf16 = args.input == "bf16-logits"
+    if bf16:  # the synthetic log-probs as bf16 logits (log-softmax is shift invariant)
+        Dd = Dd.to(torch.bfloat16)
+        args.no_e2e = True  # flexctc_decode_host takes fp32 log-probs
     Ld = torch.from_numpy(L).to(dev)
-    ws = F.make_workspace(B, T, Vp1, cfg, dev)
+    ws = FX.make_logits_workspace(B, T, Vp1, cfg, dev) if args.input == "bf16-logits" else F.make_workspace(B, T, Vp1, cfg, dev)
     stream = torch.cuda.Stream(dev)
     out = None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -260,7 +266,10 @@ def run_flexctc(args):
             if e is not None:
                 e[0].record(stream)
                 FX.set_profile_events(e[2], e[3])
-            out = F.decode(Dd, Ld, cfg, lm, bt, workspace=ws, stream=stream, outputs=out)
+            if bf16:
+                out = F.decode_logits_bf16(Dd, Ld, cfg, lm, bt, workspace=ws, stream=stream, outputs=out)
+            else:
+                out = F.decode(Dd, Ld, cfg, lm, bt, workspace=ws, stream=stream, outputs=out)
             if e is not None:
                 e[1].record(stream)
                 FX.set_profile_events(None, None)
@@ -360,6 +369,7 @@ def run_flexctc(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_dec / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "input": args.input,
             "config": workload_config(wl, B, T, frames_local, {"parallelism": f"dp{world} (utterance shards)"}),
             "frames_beams_per_s": fbps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

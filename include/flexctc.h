@@ -173,6 +173,29 @@ flexctc_status flexctc_decode_nbest(const float* log_probs, int64_t stride_b, in
                                     int32_t* out_tokens, int32_t* out_num_tokens, float* out_scores,
                                     int32_t* out_timestamps);
 
+/* ---------------------------------------------------------------------------------------
+ * flexctc_decode_logits_bf16 — flexctc_decode over bf16 LOGITS instead of fp32 log-probs
+ * (the log-softmax the acoustic model would otherwise run, moved into the
+ * decoder's input side; the bf16 input halves the bytes read from HBM and copied from the host).
+ * One bandwidth-bound pass normalises every frame t < lengths[b] (reading R25: m = max,
+ * S = sum exp(x - m) and lse = m + log S in fp64, D = (float)(x - lse)) into the workspace, then
+ * the decode runs on D exactly as flexctc_decode.
+ *   logits      device bf16 bit patterns (uint16), element (b, t, w) at
+ *               logits[b·stride_b + t·stride_t + w]; unit stride over w; NULL allowed iff T = 0.
+ *   workspace   at least flexctc_logits_workspace_bytes(B, T, Vp1, cfg) bytes (the decode's
+ *               workspace plus the dense fp32 [B, T, Vp1] log-probs).
+ * Everything else (arguments, outputs, errors, asynchrony) as flexctc_decode.
+ * ------------------------------------------------------------------------------------- */
+size_t flexctc_logits_workspace_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg);
+flexctc_status flexctc_decode_logits_bf16(const uint16_t* logits, int64_t stride_b, int64_t stride_t,
+                                          const int32_t* lengths, int32_t B, int32_t T, int32_t Vp1,
+                                          const flexctc_config* cfg, const flexctc_lm* lm,
+                                          const flexctc_boost* boost, void* workspace,
+                                          size_t workspace_bytes, flexctc_stream stream,
+                                          int32_t* out_tokens, int32_t* out_num_tokens,
+                                          float* out_scores, int32_t* out_timestamps,
+                                          int32_t* out_alignment);
+
 /* Measurement hook: when both are non-NULL, subsequent flexctc_decode calls on this thread
  * record `ev_start` (a cudaEvent_t) immediately before and `ev_stop` immediately after the
  * persistent beam kernel on the decode stream, so callers can time that kernel alone.

@@ -249,6 +249,11 @@ size_t flexctc_workspace_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_
     return workspace_layout(B, T, cfg->beam).total;
 }
 
+size_t flexctc_logits_workspace_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg) {
+    if (!cfg || B < 0 || T < 0 || Vp1 < 2 || cfg->beam < 1) return 0;
+    return workspace_layout(B, T, cfg->beam).total + (((size_t)B * T * Vp1 * 4 + 255) & ~size_t(255));
+}
+
 static flexctc_status validate_cfg(const flexctc_config* cfg) {
     if (!cfg) return fail(FLEXCTC_ERR_INVALID_ARG, "cfg is NULL");
     if (cfg->beam < 1) return fail(FLEXCTC_ERR_INVALID_ARG, "beam must be >= 1");
@@ -267,7 +272,8 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
                                   const flexctc_boost* boost, void* workspace, size_t workspace_bytes,
                                   flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
                                   float* out_scores, int32_t* out_timestamps, int32_t* out_alignment,
-                                  const uint32_t* ready, int overread, int32_t nbest = 1) {
+                                  const uint32_t* ready, int overread, int32_t nbest = 1,
+                                  const uint16_t* logits = nullptr) {
     flexctc_status st = validate_cfg(cfg);
     if (st != FLEXCTC_OK) return st;
     if (nbest < 1 || nbest > cfg->beam) return fail(FLEXCTC_ERR_INVALID_ARG, "nbest must be in [1, beam]");
@@ -277,15 +283,17 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     if (stride_t < Vp1 || stride_b < (int64_t)T * stride_t) return fail(FLEXCTC_ERR_INVALID_ARG, "strides overlap rows");
     if ((int64_t)Vp1 * cfg->beam >= (int64_t)0xffffffff) return fail(FLEXCTC_ERR_CAPACITY, "K*Vp1 too large");
     const WorkspaceLayout wl = workspace_layout(B, T, cfg->beam);
-    if (!workspace || workspace_bytes < wl.total)
-        return fail(FLEXCTC_ERR_CAPACITY, "workspace smaller than flexctc_workspace_bytes()");
+    const size_t need = wl.total + (logits ? ((size_t)B * T * Vp1 * 4 + 255) & ~size_t(255) : 0);
+    if (!workspace || workspace_bytes < need)
+        return fail(FLEXCTC_ERR_CAPACITY, logits ? "workspace smaller than flexctc_logits_workspace_bytes()"
+                                                 : "workspace smaller than flexctc_workspace_bytes()");
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (B == 0) return FLEXCTC_OK;
     // T = 0: the [B, T] arrays are empty and may be NULL (nothing is read or written there)
     auto dev_bt = [&](const void* q, bool required) { return T == 0 ? true : (q ? is_device_ptr(q, dev) : !required); };
-    if (!dev_bt(log_probs, true) || !is_device_ptr(lengths, dev) || !is_device_ptr(workspace, dev) ||
+    if (!dev_bt(logits ? (const void*)logits : (const void*)log_probs, true) || !is_device_ptr(lengths, dev) || !is_device_ptr(workspace, dev) ||
         !dev_bt(out_tokens, true) || !is_device_ptr(out_num_tokens, dev) || !is_device_ptr(out_scores, dev) ||
         !dev_bt(out_timestamps, false) || !dev_bt(out_alignment, false))
         return fail(FLEXCTC_ERR_INVALID_ARG, "every buffer must be device memory of the current device (no CPU path)");
@@ -325,6 +333,17 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.overread = overread;
     p.nbest = nbest;
     std::string err;
+    if (logits) {
+        // bf16 logits: a bandwidth-bound log-softmax pass (R25) into the workspace's dense fp32
+        // [B][T][Vp1] region, then the decode of those log-probs
+        float* Dw = (float*)((char*)workspace + wl.total);
+        const int rc0 = launch_log_softmax_bf16(logits, stride_b, stride_t, lengths, B, T, Vp1, Dw, (void*)stream, err);
+        if (rc0 == 2) return fail(FLEXCTC_ERR_CAPACITY, err);
+        if (rc0 != 0) return fail(FLEXCTC_ERR_CUDA, err);
+        p.log_probs = Dw;
+        p.stride_b = (int64_t)T * Vp1;
+        p.stride_t = Vp1;
+    }
     int rc = launch_decode(p, (void*)stream, g_ev_start, g_ev_stop, err);
     if (rc == 2) return fail(FLEXCTC_ERR_CAPACITY, err);
     if (rc != 0) return fail(FLEXCTC_ERR_CUDA, err);
@@ -348,6 +367,18 @@ flexctc_status flexctc_decode_nbest(const float* log_probs, int64_t stride_b, in
                                     int32_t* out_timestamps) {
     return decode_impl(log_probs, stride_b, stride_t, lengths, B, T, Vp1, cfg, lm, boost, workspace, workspace_bytes,
                        stream, out_tokens, out_num_tokens, out_scores, out_timestamps, nullptr, nullptr, 0, nbest);
+}
+
+flexctc_status flexctc_decode_logits_bf16(const uint16_t* logits, int64_t stride_b, int64_t stride_t,
+                                          const int32_t* lengths, int32_t B, int32_t T, int32_t Vp1,
+                                          const flexctc_config* cfg, const flexctc_lm* lm,
+                                          const flexctc_boost* boost, void* workspace, size_t workspace_bytes,
+                                          flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                                          float* out_scores, int32_t* out_timestamps, int32_t* out_alignment) {
+    if (T > 0 && !logits) return fail(FLEXCTC_ERR_INVALID_ARG, "logits is NULL");
+    return decode_impl(nullptr, stride_b, stride_t, lengths, B, T, Vp1, cfg, lm, boost, workspace, workspace_bytes,
+                       stream, out_tokens, out_num_tokens, out_scores, out_timestamps, out_alignment, nullptr, 0, 1,
+                       logits);
 }
 
 void flexctc_set_profile_events(void* ev_start, void* ev_stop) {

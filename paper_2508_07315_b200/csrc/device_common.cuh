@@ -201,6 +201,9 @@ __device__ __forceinline__ void bulk_row(float* slot, const float* src, int Vp1,
     }
 }
 
+// ---- bf16 logits input (reading R25) ---------------------------------
+__device__ __forceinline__ float bf16f(uint16_t x) { return __uint_as_float((uint32_t)x << 16); }
+
 // per-CTA device counters (SURVEY §5 "device counters"), flushed per utterance
 enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEvalDense, kCompactions,
             kStageA, kDeferredNext,

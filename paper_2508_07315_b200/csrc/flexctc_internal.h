@@ -130,6 +130,9 @@ WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K);
 // launches (beam_kernel.cu; K = 1 goes to launch_greedy in greedy_kernel.cu)
 int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
 int launch_greedy(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
+// input side (input_kernel.cu): log-softmax of bf16 logits into a dense fp32 [B][T][Vp1] buffer
+int launch_log_softmax_bf16(const uint16_t* x, int64_t stride_b, int64_t stride_t, const int32_t* lengths, int B,
+                            int T, int Vp1, float* out, void* stream, std::string& err);
 
 }  // namespace flexctc
 

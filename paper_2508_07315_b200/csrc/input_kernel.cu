@@ -1,0 +1,91 @@
+// Input side: log-softmax of bf16 logits, reading R25.
+//
+// The frame loop is latency-bound, so the normalisation is NOT fused into it (measured: doing it
+// in the helper warps per frame made c4 2.25 -> 2.78 ms, the helpers arrived late at B0). It runs
+// as one bandwidth-bound pass before the decode instead: one CTA per 8 consecutive frames of one
+// utterance, one warp per row (t < L_b only; padding is never read, R16). Per row: m = max over the
+// bf16 values (exact in fp32), S = sum exp(x - m) in fp64, lse = m + log(S) in fp64 (every lane
+// the same value), D = (float)(x - lse) written as a dense fp32 row. R25 fixes this arithmetic;
+// the fp64 sum runs in a different order than the oracle's (~1e-16 relative), so the fp32 outputs
+// agree except at a rounding boundary.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "device_common.cuh"
+#include "flexctc_internal.h"
+
+namespace flexctc {
+namespace {
+
+using namespace dev;
+
+constexpr int kRows = 8;      // frames (warps) per CTA
+constexpr int kPerLane = 33;  // register-resident elements per lane at V' <= 1056
+
+__global__ void __launch_bounds__(32 * kRows) log_softmax_bf16_kernel(const uint16_t* __restrict__ X, int64_t sb,
+                                                                     int64_t st, const int32_t* __restrict__ lengths,
+                                                                     int B, int T, int Vp1, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int nchunk = (T + kRows - 1) / kRows;
+    const int b = blockIdx.x / nchunk;
+    const int t = (blockIdx.x - b * nchunk) * kRows + (threadIdx.x >> 5);
+    const int L = min(max(__ldg(&lengths[b]), 0), T);
+    if (t >= L) return;
+    const uint16_t* x = X + (int64_t)b * sb + (int64_t)t * st;
+    float* d = out + ((int64_t)b * T + t) * Vp1;
+    if (Vp1 <= 32 * kPerLane) {  // the row in registers: one read of HBM
+        float v[kPerLane];
+#pragma unroll
+        for (int i = 0; i < kPerLane; ++i) {
+            const int w = lane + 32 * i;
+            v[i] = w < Vp1 ? bf16f(__ldcs(x + w)) : -INFINITY;
+        }
+        float m = v[0];
+#pragma unroll
+        for (int i = 1; i < kPerLane; ++i) m = fmaxf(m, v[i]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        double S = 0.0;
+#pragma unroll
+        for (int i = 0; i < kPerLane; ++i)
+            if (lane + 32 * i < Vp1) S += exp((double)v[i] - (double)m);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+        const double lse = (double)m + log(S);
+#pragma unroll
+        for (int i = 0; i < kPerLane; ++i) {
+            const int w = lane + 32 * i;
+            if (w < Vp1) d[w] = (float)((double)v[i] - lse);
+        }
+        return;
+    }
+    // larger vocabularies: three passes over the row (L2-resident after the first)
+    float m = -INFINITY;
+    for (int w = lane; w < Vp1; w += 32) m = fmaxf(m, bf16f(x[w]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double S = 0.0;
+    for (int w = lane; w < Vp1; w += 32) S += exp((double)bf16f(x[w]) - (double)m);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+    const double lse = (double)m + log(S);
+    for (int w = lane; w < Vp1; w += 32) d[w] = (float)((double)bf16f(x[w]) - lse);
+}
+
+}  // namespace
+
+int launch_log_softmax_bf16(const uint16_t* x, int64_t stride_b, int64_t stride_t, const int32_t* lengths, int B,
+                            int T, int Vp1, float* out, void* stream, std::string& err) {
+    const int64_t grid = (int64_t)B * ((T + kRows - 1) / kRows);
+    if (grid == 0) return 0;
+    if (grid > 0x7fffffff) { err = "B * T too large"; return 2; }
+    log_softmax_bf16_kernel<<<(int)grid, 32 * kRows, 0, (cudaStream_t)stream>>>(x, stride_b, stride_t, lengths, B, T,
+                                                                                 Vp1, out);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
+    return 0;
+}
+
+}  // namespace flexctc

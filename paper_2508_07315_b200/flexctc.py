@@ -51,7 +51,7 @@ EXPORTS = [
     "flexctc_last_error", "flexctc_version", "flexctc_lm_load", "flexctc_lm_free", "flexctc_lm_get_info",
     "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
     "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
-    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_decode_nbest", "flexctc_set_profile_events", "flexctc_get_stats",
+    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_decode_nbest", "flexctc_decode_logits_bf16", "flexctc_logits_workspace_bytes", "flexctc_set_profile_events", "flexctc_get_stats",
 ]
 STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
               "exact_dense", "compactions", "top_token_stages", "deferred_next",
@@ -92,6 +92,10 @@ def _declare(L: ctypes.CDLL) -> ctypes.CDLL:
                                  vp, vp, vp, vp, vp]
     L.flexctc_decode_nbest.argtypes = [vp, i64, i64, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, i32,
                                        vp, vp, vp, vp]
+    L.flexctc_logits_workspace_bytes.argtypes = [i32, i32, i32, P(Config)]
+    L.flexctc_logits_workspace_bytes.restype = sz
+    L.flexctc_decode_logits_bf16.argtypes = [vp, i64, i64, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp,
+                                             vp, vp, vp, vp, vp]
     L.flexctc_check.argtypes = [vp, P(ctypes.c_uint32)]
     L.flexctc_host_scratch_bytes.argtypes = [i32, i32, i32, P(Config)]
     L.flexctc_host_scratch_bytes.restype = sz
@@ -203,6 +207,13 @@ def make_workspace(B: int, T: int, Vp1: int, cfg: Config, device=None):
     return Workspace(torch.empty(max(n, 1), dtype=torch.uint8, device=device or "cuda"), n)
 
 
+def make_logits_workspace(B: int, T: int, Vp1: int, cfg: Config, device=None):
+    """Workspace for decode_logits_bf16 (flexctc_logits_workspace_bytes)."""
+    import torch
+    n = int(lib.flexctc_logits_workspace_bytes(int(B), int(T), int(Vp1), ctypes.byref(cfg)))
+    return Workspace(torch.empty(max(n, 1), dtype=torch.uint8, device=device or "cuda"), n)
+
+
 def decode(log_probs, lengths, cfg: Config, lm: LM | None = None, boost: Boost | None = None,
            Vp1: int | None = None, workspace: Workspace | None = None, stream=None, outputs=None,
            alignment: bool = False):
@@ -272,6 +283,40 @@ def decode_nbest(log_probs, lengths, cfg: Config, nbest: int, lm: LM | None = No
                                         int(nbest), _ptr(out["tokens"]), _ptr(out["num_tokens"]), _ptr(out["scores"]),
                                         _ptr(out["timestamps"])))
     return out
+
+
+def decode_logits_bf16(logits, lengths, cfg: Config, lm: LM | None = None, boost: Boost | None = None,
+                       Vp1: int | None = None, workspace: Workspace | None = None, stream=None, outputs=None,
+                       alignment: bool = False):
+    """Enqueue flexctc_decode_logits_bf16: like decode() but over bf16 logits [B, T, >=Vp1]
+    (torch.bfloat16, unit stride on the last axis), normalised on the GPU (reading R25) first."""
+    import torch
+    if not (logits.is_cuda and lengths.is_cuda):
+        raise FlexCTCError(1, "decode needs CUDA tensors (there is no CPU path)")
+    if logits.dtype != torch.bfloat16 or logits.dim() != 3 or logits.stride(2) != 1:
+        raise FlexCTCError(1, "logits must be bfloat16 [B, T, V'] with unit stride on V'")
+    B, T, W = logits.shape
+    Vp1 = W if Vp1 is None else Vp1
+    dev = logits.device
+    if workspace is None:
+        workspace = make_logits_workspace(B, T, Vp1, cfg, dev)
+    if outputs is None:
+        outputs = {"tokens": torch.empty((B, T), dtype=torch.int32, device=dev),
+                   "num_tokens": torch.empty(B, dtype=torch.int32, device=dev),
+                   "scores": torch.empty(B, dtype=torch.float32, device=dev),
+                   "timestamps": torch.empty((B, T), dtype=torch.int32, device=dev)}
+        if alignment:
+            outputs["alignment"] = torch.empty((B, T), dtype=torch.int32, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        _check(lib.flexctc_decode_logits_bf16(_ptr(logits), logits.stride(0), logits.stride(1), _ptr(lengths), B, T,
+                                              Vp1, ctypes.byref(cfg), lm.h if lm else None,
+                                              boost.h if boost else None, _ptr(workspace.buf), workspace.nbytes,
+                                              ctypes.c_void_p(stream.cuda_stream), _ptr(outputs["tokens"]),
+                                              _ptr(outputs["num_tokens"]), _ptr(outputs["scores"]),
+                                              _ptr(outputs.get("timestamps")), _ptr(outputs.get("alignment"))))
+    return outputs
 
 
 def set_profile_events(start=None, stop=None):

@@ -384,6 +384,9 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
             {
                 const int r = t + kGRing - 1;
                 if (r < L) {
+                    // every lane's reads of this slot (frame t - 1) precede lane 0's proxy fence and the
+                    // async-proxy (TMA) write that reuses it
+                    __syncwarp();
                     wait_ready(p, r, ready);
                     bulk_row(ring + (size_t)(r % kGRing) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1,
                              &bar[r % kGRing], lo, hi, lane);

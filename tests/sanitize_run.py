@@ -2,8 +2,10 @@
 
   compute-sanitizer --tool racecheck python tests/sanitize_run.py
 
-Covers the beam-warp + helpers mode (K <= 32, LM + boosting), the whole-CTA mode (K = 64) and the
-single-warp launch, on a few short utterances, and checks the results against the oracle."""
+Covers the beam-warp + helpers mode (K <= 32, LM + boosting), the whole-CTA mode (K = 64), the
+single-warp launch, the greedy kernels (plain and fused, K = 1; TMA bulk rows + mbarriers), the
+n-best output, the bf16-logits input pass and the streamed host path, on a few short utterances,
+and checks the results against the oracle."""
 import os
 import sys
 
@@ -37,7 +39,47 @@ def run(K, nt=None):
     print(f"K={K} nt={nt or 'default'} ok")
 
 
+def run_more():
+    os.environ.pop("FLEXCTC_NT", None)
+    L = np.array([40, 17, 0, 33], dtype=np.int32)
+    ph = synth.phrases(1024)
+    D, _ = synth.logprobs(4, 40, 1024, L, 5, ph)
+    arpa = synth.arpa_file(V=1024)
+    glm, gbt = F.LM(arpa, 1024, device=0), F.Boost(ph, 1.0, 1024, device=0)
+    olm, obt = oracle.LM(arpa, 1024), oracle.Boost(ph, 1.0, 1024)
+    Dt, Lt = torch.from_numpy(D).cuda(), torch.from_numpy(L).cuda()
+
+    def check(out, ref, what):
+        assert np.array_equal(out["tokens"].cpu().numpy(), ref["tokens"]), what
+        assert np.allclose(out["scores"].cpu().numpy(), ref["scores"], atol=1e-4), what
+        print(what, "ok")
+
+    for cfg, lm, bt in ((F.config(1), None, None), (F.config(1, 0.5, 1.0, 0.5, 12.0), glm, gbt)):
+        out = F.decode(Dt, Lt, cfg, lm, bt)
+        torch.cuda.synchronize()
+        ref = oracle.decode(D, L, oracle.make_cfg(1, cfg.alpha_lm, cfg.alpha_bt, cfg.beta, 12.0),
+                            olm if lm else None, obt if bt else None, nthreads=4)
+        check(out, ref, f"greedy lm={lm is not None}")
+    cfg = F.config(16, 0.5, 1.0, 0.5, 12.0)
+    ref = oracle.decode(D, L, oracle.make_cfg(16, 0.5, 1.0, 0.5, 12.0), olm, obt, nthreads=4)
+    nb = F.decode_nbest(Dt, Lt, cfg, 4, glm, gbt)
+    torch.cuda.synchronize()
+    check({"tokens": nb["tokens"][:, 0], "scores": nb["scores"][:, 0]}, ref, "nbest")
+    hout = F.decode_host(torch.from_numpy(D).pin_memory(), torch.from_numpy(L).pin_memory(), cfg, glm, gbt)
+    check(hout, ref, "decode_host streamed")
+    u = D.view(np.uint32).astype(np.uint64)
+    bits = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    Dq = oracle.log_softmax_bf16(bits)
+    x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    for K in (16, 1):
+        out = F.decode_logits_bf16(x, Lt, F.config(K, 0.5, 1.0, 0.5, 12.0), glm, gbt)
+        torch.cuda.synchronize()
+        check(out, oracle.decode(Dq, L, oracle.make_cfg(K, 0.5, 1.0, 0.5, 12.0), olm, obt, nthreads=4),
+              f"logits bf16 K={K}")
+
+
 if __name__ == "__main__":
     run(16)
     run(64)
     run(16, nt=32)
+    run_more()

@@ -283,13 +283,13 @@ __global__ void __launch_bounds__(128) greedy_chain_kernel(const DecodeParams p)
 
 // ---------------------------------------------------------------------------------- fused path
 
-constexpr int kGW = 4;     // utterances (warps) per CTA
-constexpr int kGRing = 8;  // frame rows in flight per warp (covers HBM latency at ~300-cycle frames)
+constexpr int kGW = 4;     // utterances (warps) per CTA, at most (fewer when V' makes the ring large)
+constexpr int kGRing = 8;  // frame rows in flight per warp, at most (covers HBM latency at ~300-cycle frames)
 
-__host__ __device__ __forceinline__ size_t greedy_warp_smem(int Vp1, int RWS) {
+__host__ __device__ __forceinline__ size_t greedy_warp_smem(int Vp1, int RWS, int ring) {
     const int VP = (Vp1 + 3) & ~3;
-    const size_t a = (((size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)Vp1 * 2 + 7) & ~size_t(7));
-    return (a + 8 * kGRing + 15) & ~size_t(15);
+    const size_t a = (((size_t)ring * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)Vp1 * 2 + 7) & ~size_t(7));
+    return (a + 8 * (size_t)ring + 15) & ~size_t(15);
 }
 
 __device__ __forceinline__ float4 shfl4(float4 v, int src) {
@@ -298,7 +298,7 @@ __device__ __forceinline__ float4 shfl4(float4 v, int src) {
 }
 
 template <int LMV>
-__global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodeParams p, const int ringn /* 2, 4 or 8 */) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int Vp1 = p.Vp1, blank = Vp1 - 1, V = Vp1 - 1;
@@ -306,19 +306,19 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
     const int RWS = lm_on ? ((p.lm.RW + 3) & ~3) : 4;
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
-    // layout: [kGW] x {ring[kGRing][VP + 4] f32, rec[RWS] i32, list[Vp1] u16, bar[kGRing] u64},
+    // layout: [warps] x {ring[ringn][VP + 4] f32, rec[RWS] i32, list[Vp1] u16, bar[ringn] u64},
     // then btroot[V] int2
-    const size_t per_warp = greedy_warp_smem(Vp1, RWS);
+    const size_t per_warp = greedy_warp_smem(Vp1, RWS, ringn);
     unsigned char* base = smem_raw + (size_t)wid * per_warp;
     float* ring = (float*)base;
-    int* rec = (int*)(base + (size_t)kGRing * (VP + 4) * 4);
-    uint16_t* list = (uint16_t*)(base + (size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4);
-    uint64_t* bar = (uint64_t*)(base + (((size_t)kGRing * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)Vp1 * 2 + 7) & ~size_t(7)));
-    int2* btroot = (int2*)(smem_raw + (size_t)kGW * per_warp);
+    int* rec = (int*)(base + (size_t)ringn * (VP + 4) * 4);
+    uint16_t* list = (uint16_t*)(base + (size_t)ringn * (VP + 4) * 4 + (size_t)RWS * 4);
+    uint64_t* bar = (uint64_t*)(base + (((size_t)ringn * (VP + 4) * 4 + (size_t)RWS * 4 + (size_t)Vp1 * 2 + 7) & ~size_t(7)));
+    int2* btroot = (int2*)(smem_raw + (size_t)(blockDim.x >> 5) * per_warp);
     if (bt_on)
         for (int w = threadIdx.x; w < V; w += blockDim.x) btroot[w] = __ldg(&p.bt.tab[w]);
     if (lane == 0) {
-        for (int i = 0; i < kGRing; ++i) mbar_init(&bar[i], 1);
+        for (int i = 0; i < ringn; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -369,39 +369,39 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
         const float4 none4 = make_float4(kNeg, kNeg, kNeg, __uint_as_float(0xffffffffu));
         float4 sum_c = lane < L ? summ[lane] : none4;
         float4 sum_n = 32 + lane < L ? summ[32 + lane] : none4;
-        // frame rows: one TMA bulk copy per row (lane 0), kGRing - 1 rows ahead
+        // frame rows: one TMA bulk copy per row (lane 0), ringn - 1 rows ahead
         int nissued = 0, ncons = 0;
-        for (int r = 0; r < kGRing - 1 && r < L; ++r) {
+        for (int r = 0; r < ringn - 1 && r < L; ++r) {
             wait_ready(p, r, ready);
             bulk_row(ring + (size_t)r * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, &bar[r], lo, hi, lane);
         }
-        nissued = min(kGRing - 1, L);
+        nissued = min(ringn - 1, L);
         for (int t = 0; t < L; ++t) {
             if ((t & 31) == 0 && t) {
                 sum_c = sum_n;
                 sum_n = t + 32 + lane < L ? summ[t + 32 + lane] : none4;
             }
             {
-                const int r = t + kGRing - 1;
+                const int r = t + ringn - 1;
                 if (r < L) {
                     // every lane's reads of this slot (frame t - 1) precede lane 0's proxy fence and the
                     // async-proxy (TMA) write that reuses it
                     __syncwarp();
                     wait_ready(p, r, ready);
-                    bulk_row(ring + (size_t)(r % kGRing) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1,
-                             &bar[r % kGRing], lo, hi, lane);
+                    bulk_row(ring + (size_t)(r & (ringn - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1,
+                             &bar[r & (ringn - 1)], lo, hi, lane);
                     nissued = r + 1;
                 }
             }
             const float4 fs4 = shfl4(sum_c, t & 31);
             const int w1 = (int)(__float_as_uint(fs4.w) & 0xffffu);
             {
-                const int sl = t % kGRing;
+                const int sl = t & (ringn - 1);
                 mbar_wait(&bar[sl], (ph >> sl) & 1u);
                 ph ^= 1u << sl;
                 ncons = t + 1;
             }
-            const float* row = ring + (size_t)(t % kGRing) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
+            const float* row = ring + (size_t)(t & (ringn - 1)) * (VP + 4) + row_off(Db + (int64_t)t * p.stride_t);
             // exact blank / repeat candidates: no β, no fusion
             uint64_t best = 0;
             int best_ln = lms, best_bn = bts;
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
             last = ws;
         }
         for (int f = ncons; f < nissued; ++f) {  // rows issued past a dead frame: drain the ring
-            const int sl = f % kGRing;
+            const int sl = f & (ringn - 1);
             mbar_wait(&bar[sl], (ph >> sl) & 1u);
             ph ^= 1u << sl;
         }
@@ -531,20 +531,25 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
 template <int LMV>
 int launch_fused(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
     const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
-    const size_t per_warp = greedy_warp_smem(p.Vp1, RWS);
-    const size_t smem = kGW * per_warp + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0);
+    // ring depth and warps per CTA: the deepest ring (<= 8 rows) and the most warps (<= 4) that fit
+    // 200 KB of shared memory (V' up to 8192: 2 rows x 1 warp)
+    const size_t root = p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0;
+    int ringn = kGRing, gw = kGW;
+    while (ringn > 2 && greedy_warp_smem(p.Vp1, RWS, ringn) + root > 200 * 1024) ringn >>= 1;
+    while (gw > 1 && gw * greedy_warp_smem(p.Vp1, RWS, ringn) + root > 200 * 1024) --gw;
+    const size_t smem = gw * greedy_warp_smem(p.Vp1, RWS, ringn) + root;
     if (smem > 200 * 1024) { err = "shared memory requirement too large (V+1)"; return 2; }
     auto kern = greedy_fused_kernel<LMV>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kGW, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * gw, smem);
     if (e != cudaSuccess || occ < 1) { err = e != cudaSuccess ? cudaGetErrorString(e) : "occupancy query failed"; return 1; }
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min((p.B + kGW - 1) / kGW, nsm * occ);
+    const int grid = std::min((p.B + gw - 1) / gw, nsm * occ);
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-    kern<<<grid, 32 * kGW, smem, st>>>(p);
+    kern<<<grid, 32 * gw, smem, st>>>(p, ringn);
     e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }

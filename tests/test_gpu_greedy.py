@@ -113,3 +113,19 @@ def test_greedy_zero_frames(lm_pair):
         assert g["tokens"].shape == (3, 0)
         assert g["num_tokens"].tolist() == [0, 0, 0] == o["num_tokens"].tolist()
         assert np.array_equal(g["scores"].view(np.int32), o["scores"].view(np.int32))
+
+
+@pytest.mark.parametrize("Vp1", [4097, 5000, 8192])
+def test_large_vocab_greedy_and_beam(Vp1):
+    """V' beyond one 16-B-load batch per lane (frame_summary_kernel folds the arg-max across
+    batches) and up to the 8192 limit; the fused path and the beam kernel at the same size."""
+    rng = np.random.default_rng(Vp1)
+    B, T = 3, 24
+    D = synth.random_logprobs(rng, B, T, Vp1, peak=8.0).astype(np.float32)
+    D[0, 5, 4100:4110] = D[0, 5].max()  # exact ties of the max in the second batch region
+    D[1, 7, [3, Vp1 - 40]] = D[1, 7].max() + 1.0  # the max in the first and the second batch
+    L = [24, 24, 9]
+    for cfg in (F.config(1), F.config(1, beta=0.3), F.config(4, theta=12.0)):
+        g = gpu_decode(D, L, cfg)
+        o = oracle.decode(D, L, ocfg(cfg), nthreads=1, with_alignment=True)
+        compare(g, o, bitwise=cfg.beam == 1)

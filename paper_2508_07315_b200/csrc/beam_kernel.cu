@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             for (int r = 0; r < pf; ++r) {  // prologue
                 if (r < L) {
                     wait_ready(p, r, ready);
-                    load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                    load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
                 }
                 cp_commit();
             }
@@ -433,14 +433,14 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const Bank cur = bank(cb);
             const Bank nxt = bank(cb ^ 1);
             const long long ctop = TCLK();
-            const int slot = t % R;
+            const int slot = t & (R - 1);  // R is 4 or 2
             float* ring_t = sm.ring + (size_t)slot * (VP + 4);
             const float* row = ring_t + row_off(Db + (int64_t)t * p.stride_t);
             if (!solo || helper) {
                 const int r = t + pf;
                 if (r < L) {
                     wait_ready(p, r, ready);
-                    load_row(sm.ring + (size_t)(r % R) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                    load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
                 }
                 cp_commit();
                 if (solo) cp_wait<2>(); else if (R == 4) cp_wait<3>(); else cp_wait<1>();

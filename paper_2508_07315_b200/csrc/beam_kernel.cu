@@ -282,7 +282,10 @@ __device__ void build_lm_row(const LmDev& lm, int state, float* row, int V) {
     }
 }
 
-template <int NT, int LMV>
+// SOLO (K <= 32, NT >= 128, 4-row ring; chosen on the host): warp 0 is the beam warp, the other
+// warps are helpers. A template parameter so the group size of the slot-parallel phases is a
+// compile-time constant.
+template <int NT, int LMV, bool SOLO>
 __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
                                                       const int nrow, const int dense_min) {
     constexpr int kRec = (8 + 3 * LMV + 3) & ~3;  // ints per cached LM record
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
     const int RWS = lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
-    const bool solo = K <= 32 && NT >= 128 && R == kRing && !p.solo_off;  // >= 3 helper warps
+    constexpr bool solo = SOLO;  // host: K <= 32 && NT >= 128 && R == kRing && !solo_off (>= 3 helper warps)
     const bool helper = solo && tid >= 32;
     const bool bw = !solo || tid < 32;               // takes part in the slot-serial phases
     const int ltid = helper ? tid - 32 : tid;        // row loader index / count
@@ -1162,7 +1165,7 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
     const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
     pl.sm = smem_bytes(p.K, p.Vp1, pl.R, pl.cap, p.nch, RWS) + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) + 16 : 0);
     if (pl.sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
-    auto kern = ctc_beam_kernel<NT, LMV>;
+    auto kern = ctc_beam_kernel<NT, LMV, false>;
     cudaFuncAttributes fattr{};
     cudaFuncGetAttributes(&fattr, kern);
     // The dense-frame LM row cache is off by default: with 8 warps per utterance the batched
@@ -1180,6 +1183,10 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
         pl.sm += pl.nrow ? 4 * (size_t)pl.nrow * VP + ((4 * (size_t)pl.nrow + 15) & ~size_t(15)) : 0;
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
+    if constexpr (NT >= 128)
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)pl.sm);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.occ, kern, NT, pl.sm);
     if (e != cudaSuccess || pl.occ < 1) { err = "occupancy query failed"; return 1; }
@@ -1188,13 +1195,19 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
 
 template <int NT, int LMV>
 int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
-    auto kern = ctc_beam_kernel<NT, LMV>;
     const int grid = std::min(p.B, nsm * pl.occ);
     DecodeParams q = p;
     const char* e_solo = getenv("FLEXCTC_SOLO");  // "0": every phase uses the whole CTA (test switch)
     q.solo_off = (e_solo && e_solo[0] == '0') ? 1 : 0;
+    const bool solo = p.K <= 32 && NT >= 128 && pl.R == 4 && !q.solo_off;  // 4 = the kernel's kRing
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-    kern<<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+    if constexpr (NT >= 128) {
+        if (solo) ctc_beam_kernel<NT, LMV, true><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+        else ctc_beam_kernel<NT, LMV, false><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+    } else {
+        (void)solo;
+        ctc_beam_kernel<NT, LMV, false><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+    }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }

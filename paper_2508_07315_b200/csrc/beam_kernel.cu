@@ -1187,10 +1187,14 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pl.sm);
-    if constexpr (NT == 256 && LMV == 2)
+    if constexpr (NT == 256 && LMV == 2) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pl.sm);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, false, 1025>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)pl.sm);
+    }
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.occ, kern, NT, pl.sm);
     if (e != cudaSuccess || pl.occ < 1) { err = "occupancy query failed"; return 1; }
@@ -1207,9 +1211,10 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
     if constexpr (NT >= 128) {
         bool done = false;
-        if constexpr (NT == 256 && LMV == 2)  // the paper's vocabulary (1024 BPE tokens + blank), K <= 32
-            if (solo && p.Vp1 == 1025) {
-                ctc_beam_kernel<NT, LMV, true, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+        if constexpr (NT == 256 && LMV == 2)  // the paper's vocabulary (1024 BPE tokens + blank)
+            if (p.Vp1 == 1025) {
+                if (solo) ctc_beam_kernel<NT, LMV, true, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                else ctc_beam_kernel<NT, LMV, false, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 done = true;
             }
         if (done) {

@@ -285,8 +285,8 @@ __device__ void build_lm_row(const LmDev& lm, int state, float* row, int V) {
 // SOLO (K <= 32, NT >= 128, 4-row ring; chosen on the host): warp 0 is the beam warp, the other
 // warps are helpers. A template parameter so the group size of the slot-parallel phases is a
 // compile-time constant.
-// compile-time V', K, LM record width (0 = runtime)
-template <int NT, int LMV, bool SOLO, int VPC = 0, int KC = 0, int RWC = 0>
+// compile-time V', K, LM record width (0 = runtime), fusion terms (FUS: 0 = runtime, 3 = LM + boost)
+template <int NT, int LMV, bool SOLO, int VPC = 0, int KC = 0, int RWC = 0, int FUS = 0>
 __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
                                                       const int nrow, const int dense_min) {
     constexpr int kRec = (8 + 3 * LMV + 3) & ~3;  // ints per cached LM record
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const int K = KC ? KC : p.K, Vp1 = VPC ? VPC : p.Vp1, blank = Vp1 - 1, V = Vp1 - 1;
     const int VP = (Vp1 + 3) & ~3;
     const int R = ring_rows;
-    const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
+    const bool lm_on = FUS ? (FUS & 1) != 0 : p.use_lm != 0, bt_on = FUS ? (FUS & 2) != 0 : p.use_bt != 0;
     const int RWS = RWC ? RWC : lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
     constexpr bool solo = SOLO;  // host: K <= 32 && NT >= 128 && R == kRing && !solo_off (>= 3 helper warps)
@@ -1198,6 +1198,9 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
     }
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.occ, kern, NT, pl.sm);
@@ -1217,7 +1220,9 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
         bool done = false;
         if constexpr (NT == 256 && LMV == 2)  // the paper's vocabulary (1024 BPE tokens + blank)
             if (p.Vp1 == 1025) {
-                if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16)  // beam 16 + 4-gram LM (north star)
+                if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt)  // beam 16, 4-gram LM, boosting
+                    ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 3><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16)  // beam 16 + 4-gram LM
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo) ctc_beam_kernel<NT, LMV, true, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else ctc_beam_kernel<NT, LMV, false, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);

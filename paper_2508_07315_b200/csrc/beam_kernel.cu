@@ -285,10 +285,11 @@ __device__ void build_lm_row(const LmDev& lm, int state, float* row, int V) {
 // SOLO (K <= 32, NT >= 128, 4-row ring; chosen on the host): warp 0 is the beam warp, the other
 // warps are helpers. A template parameter so the group size of the slot-parallel phases is a
 // compile-time constant.
-// compile-time V', K, LM record width (0 = runtime), fusion terms (FUS: 0 = runtime, 3 = LM + boost)
+// compile-time V', K, LM record width (0 = runtime); FUS (0 = runtime): bit 0 LM, bit 1 boosting,
+// bit 2 "plain" = no LM-row cache (nrow 0), log-sum-exp merges, non-negative fusion weights
 template <int NT, int LMV, bool SOLO, int VPC = 0, int KC = 0, int RWC = 0, int FUS = 0>
 __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
-                                                      const int nrow, const int dense_min) {
+                                                      int nrow, const int dense_min) {
     constexpr int kRec = (8 + 3 * LMV + 3) & ~3;  // ints per cached LM record
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Scalars sc;
@@ -324,7 +325,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const int R = ring_rows;
     const bool lm_on = FUS ? (FUS & 1) != 0 : p.use_lm != 0, bt_on = FUS ? (FUS & 2) != 0 : p.use_bt != 0;
     const int RWS = RWC ? RWC : lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
-    const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
+    constexpr bool plain = (FUS & 4) != 0;
+    const bool ub_inf = plain ? false : (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
+    const int merge_mode = plain ? 0 : p.merge_mode;
+    if (plain) nrow = 0;
     constexpr bool solo = SOLO;  // host: K <= 32 && NT >= 128 && R == kRing && !solo_off (>= 3 helper warps)
     const bool helper = solo && tid >= 32;
     const bool bw = !solo || tid < 32;               // takes part in the slot-serial phases
@@ -658,7 +662,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         build_lm_row<NT>(p.lm, s_build[2 * i + 1], rowval + (size_t)s_build[2 * i] * VP, V);
                     __syncthreads();
                     if (tid == 0) st[kCycRows] += (uint32_t)(TCLK() - cr);
-                } else if (m > 0) {
+                } else if (m > 0 && nrow > 0) {
                     for (int a2 = tid; a2 < nalive; a2 += G4) s_line[a2] = -1;
                 }
                 if (m > 0) {
@@ -706,7 +710,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 if (w == __float_as_int(ps.w)) continue;  // repeat: scored in phase 1
                                 const float s0 = __fadd_rn(ps.x, dw);
                                 if (__fadd_rn(s0, ps.y) + 1e-5f * (1.0f + fabsf(s0) + ps.z) < thr) continue;
-                                const int line = s_line[a2];
+                                const int line = nrow > 0 ? s_line[a2] : -1;
                                 if (line >= 0) {  // exact LM value from the cached row tightens the bound
                                     const float x = p.alpha_lm * rowval[(size_t)line * VP + w];
                                     const float ub = __fadd_rn(s_ubnl[a2], x);
@@ -736,7 +740,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 const int a2 = (int)(pq >> 16), jq = (int)(pq & 0xffffu);
                                 const int k = sm.alive_idx[a2];
                                 const int wq = sm.toks[jq];
-                                const int line = s_line[a2];
+                                const int line = nrow > 0 ? s_line[a2] : -1;
                                 const float s0 = __fadd_rn(s_pos[a2].x, row[wq]);
                                 int ln, bn;
                                 const float s = eval(cur, k, s0, wq, ln, bn, line >= 0 ? rowval + (size_t)line * VP : nullptr);
@@ -879,7 +883,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         s = kNeg;  // a better (lower) slot of the group survives
                     } else {
                         unsigned others = grp & ~((2u << i) - 1u);  // higher slots, ascending order
-                        if (others && p.merge_mode == 0) {
+                        if (others && merge_mode == 0) {
                             float sum = 0.0f;
                             while (others) {
                                 const int j = __ffs(others) - 1;
@@ -902,7 +906,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 if (mem[r] < mem[r - 1]) { const int x = mem[r]; mem[r] = mem[r - 1]; mem[r - 1] = x; }
                         if (mem[0] != i) {
                             s = kNeg;
-                        } else if (p.merge_mode == 0) {
+                        } else if (merge_mode == 0) {
                             float sum = 0.0f;
 #pragma unroll
                             for (int q = 1; q < kTabMem; ++q)
@@ -926,10 +930,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                             const float sj = nxt.acc[j];
                             if (sj > kNeg && nxt.hash[j] == h && nxt.last[j] == l) {
                                 any = true;
-                                if (p.merge_mode == 0) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(sj, s)));
+                                if (merge_mode == 0) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(sj, s)));
                             }
                         }
-                        if (any && p.merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
+                        if (any && merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
                     }
                 }
                 t7b = TCLK();
@@ -1016,11 +1020,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     }
                     if (bj < 0) break;
                     any = true;
-                    if (p.merge_mode == 0) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(bs, s)));
+                    if (merge_mode == 0) sum = __fadd_rn(sum, (float)exp((double)__fsub_rn(bs, s)));
                     prev_s = bs;
                     prev_j = bj;
                 }
-                if (any && p.merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
+                if (any && merge_mode == 0) s = __fadd_rn(s, (float)log1p((double)sum));
                 mykey = ((uint64_t)ord_of(s) << 32) | (uint64_t)(0xffffffffu - (uint32_t)i);
             }
         }
@@ -1201,6 +1205,9 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 3>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
     }
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.occ, kern, NT, pl.sm);
@@ -1220,7 +1227,11 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
         bool done = false;
         if constexpr (NT == 256 && LMV == 2)  // the paper's vocabulary (1024 BPE tokens + blank)
             if (p.Vp1 == 1025) {
-                if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt)  // beam 16, 4-gram LM, boosting
+                const bool plain = pl.nrow == 0 && p.merge_mode == 0 && !p.retract && p.alpha_lm >= 0.0f &&
+                                   p.alpha_bt >= 0.0f;
+                if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // the north-star decode
+                    ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt)  // beam 16, 4-gram LM, boosting
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 3><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16)  // beam 16 + 4-gram LM
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);

@@ -1208,6 +1208,9 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 5>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
     }
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.occ, kern, NT, pl.sm);
@@ -1231,6 +1234,8 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
                                    p.alpha_bt >= 0.0f;
                 if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // the north-star decode
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && !p.use_bt && plain)  // LM only (c3)
+                    ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 5><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt)  // beam 16, 4-gram LM, boosting
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 3><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16)  // beam 16 + 4-gram LM

@@ -679,10 +679,23 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     }
                     gsync(G4);
                     // suffix maxima of acc and |ub terms| over live positions (early exit below)
-                    for (int a2 = tid; a2 < nalive; a2 += G4) {
-                        float am = kNeg, um = 0.0f;
-                        for (int q = a2; q < nalive; ++q) { am = fmaxf(am, s_pos[q].x); um = fmaxf(um, s_pos[q].z); }
-                        s_suf[a2] = make_float2(am, um);
+                    if (solo) {  // nalive <= 32: one warp-level suffix scan in warp 0
+                        if (tid < 32) {
+                            float am = tid < nalive ? s_pos[tid].x : kNeg, um = tid < nalive ? s_pos[tid].z : 0.0f;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const float a_ = __shfl_down_sync(0xffffffffu, am, o);
+                                const float u_ = __shfl_down_sync(0xffffffffu, um, o);
+                                if (tid + o < 32) { am = fmaxf(am, a_); um = fmaxf(um, u_); }
+                            }
+                            if (tid < nalive) s_suf[tid] = make_float2(am, um);
+                        }
+                    } else {
+                        for (int a2 = tid; a2 < nalive; a2 += G4) {
+                            float am = kNeg, um = 0.0f;
+                            for (int q = a2; q < nalive; ++q) { am = fmaxf(am, s_pos[q].x); um = fmaxf(um, s_pos[q].z); }
+                            s_suf[a2] = make_float2(am, um);
+                        }
                     }
                     gsync(G4);
                     long long c4c = TCLK();

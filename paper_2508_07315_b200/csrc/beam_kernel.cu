@@ -1224,6 +1224,9 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 5>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, false, 1025, 0, 16, 7>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
     }
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.occ, kern, NT, pl.sm);
@@ -1254,6 +1257,8 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
                 else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16)  // beam 16 + 4-gram LM
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo) ctc_beam_kernel<NT, LMV, true, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                else if (p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // K > 32, 4-gram LM, boosting (c5)
+                    ctc_beam_kernel<NT, LMV, false, 1025, 0, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else ctc_beam_kernel<NT, LMV, false, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 done = true;
             }

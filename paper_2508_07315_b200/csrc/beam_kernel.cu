@@ -107,8 +107,9 @@ __device__ __forceinline__ float block_max(float v, Scalars& sc, int G) {
 
 // Phase-1 reduction in one round: max of three floats, max of a u64 key, exclusive scan of a
 // 0/1 flag (slot order). Returns via references.
+// k_uniform: k is already the same on every lane (the helpers' frame summary): not reduced.
 __device__ __forceinline__ void block_reduce_p1(float& a, float& b, float& c, uint64_t& k, bool flag, int& off,
-                                                int& tot, Scalars& sc, int G) {
+                                                int& tot, Scalars& sc, int G, bool k_uniform = false) {
     const int NW = G >> 5;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -116,7 +117,7 @@ __device__ __forceinline__ void block_reduce_p1(float& a, float& b, float& c, ui
         a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
         b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
         c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, o));
-        k = umax64(k, __shfl_xor_sync(0xffffffffu, k, o));
+        if (!k_uniform) k = umax64(k, __shfl_xor_sync(0xffffffffu, k, o));
     }
     const unsigned bal = __ballot_sync(0xffffffffu, flag);
     const int in_warp = __popc(bal & ((1u << lane) - 1u));
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 }
                 float mxrb = fmaxf(sbk, srk), accmax = a, ubvmax = ubk;
                 int aoff, nalive;
-                block_reduce_p1(mxrb, accmax, ubvmax, best_tok, al, aoff, nalive, sc, G);
+                block_reduce_p1(mxrb, accmax, ubvmax, best_tok, al, aoff, nalive, sc, G, solo);
                 if (al) sm.alive_idx[aoff] = tid;
                 wstar = (int)flat_of(best_tok);
                 const float dstar = score_of(best_tok);

@@ -806,6 +806,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             // ------------------------------------------------ phase 6: beams.update into nxt
             const int64_t bpo = bp_base + (int64_t)(t * K);
             bool live = false, emit = false;
+            float my_acc = kNeg;  // this lane's new slot (phase 7 reads it from registers)
+            int my_last = blank;
+            uint64_t my_hash = 0ull;
             int par = 0;
             int4 rec_ld[kRec / 4];
             float2 bt_ld = make_float2(0.0f, 0.0f);
@@ -833,9 +836,12 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                     if (4 * q < RWS) rec_ld[q] = __ldg(&p.lm.rec[(size_t)ln * (p.lm.RW / 4) + q]);
                             if (bt_on) bt_ld = make_float2(__ldg(&p.bt.maxd[bn]), __ldg(&p.bt.U[bn]));
                         }
-                        nxt.acc[i] = s;
-                        nxt.last[i] = w;
-                        nxt.hash[i] = emit ? hash_extend(cur.hash[par], w) : cur.hash[par];
+                        my_acc = s;
+                        my_last = w;
+                        my_hash = emit ? hash_extend(cur.hash[par], w) : cur.hash[par];
+                        nxt.acc[i] = my_acc;
+                        nxt.last[i] = my_last;
+                        nxt.hash[i] = my_hash;
                         nxt.lms[i] = ln;  // rb candidates carry the parent's states
                         nxt.bts[i] = bn;
                         nxt.anc[i] = (t % kChunk == 0) ? (uint8_t)par : cur.anc[par];
@@ -858,9 +864,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const bool small_beam = K <= 32;  // all slots live in warp 0
             if (small_beam && tid < 32) {
                 // one warp holds the beam: group lanes by (hash, last) with match.any
-                const bool lv = tid < K && nxt.acc[tid] > kNeg;
-                const uint64_t hk = lv ? nxt.hash[tid] : (0xfedcba9800000000ull | (uint64_t)tid);
-                const int lkey = lv ? nxt.last[tid] : -1 - tid;
+                const bool lv = tid < K && my_acc > kNeg;
+                const uint64_t hk = lv ? my_hash : (0xfedcba9800000000ull | (uint64_t)tid);
+                const int lkey = lv ? my_last : -1 - tid;
                 const unsigned livemask = __ballot_sync(0xffffffffu, lv);
                 // only the live lanes take part: match.any costs ~14 cycles per distinct value
                 // (444 cycles for 32 distinct 64-bit keys, tools/micro/lat.cu), and dead lanes

@@ -808,6 +808,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             bool live = false, emit = false;
             float my_acc = kNeg;  // this lane's new slot (phase 7 reads it from registers)
             int my_last = blank;
+            uint8_t my_anc = 0;
             uint64_t my_hash = 0ull;
             int par = 0;
             int4 rec_ld[kRec / 4];
@@ -844,7 +845,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         nxt.hash[i] = my_hash;
                         nxt.lms[i] = ln;  // rb candidates carry the parent's states
                         nxt.bts[i] = bn;
-                        nxt.anc[i] = (t % kChunk == 0) ? (uint8_t)par : cur.anc[par];
+                        my_anc = (t % kChunk == 0) ? (uint8_t)par : cur.anc[par];
+                        nxt.anc[i] = my_anc;
                         p.bp_parent[bpo + i] = (uint8_t)par;
                         p.bp_label[bpo + i] = (uint16_t)w;
                     }
@@ -897,7 +899,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             long long t7b = t7a, t7c = t7a;
             if (tid < K) {
                 const int i = tid;
-                float s = nxt.acc[i];
+                float s = my_acc;
                 if (small_beam && s > kNeg) {
                     if (grp & ((1u << i) - 1u)) {
                         s = kNeg;  // a better (lower) slot of the group survives
@@ -958,7 +960,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 }
                 t7b = TCLK();
                 if ((t % kChunk) == kChunk - 1 || t == L - 1)
-                    p.chunk_anc[((int64_t)b * p.nch + t / kChunk) * K + i] = nxt.anc[i];
+                    p.chunk_anc[((int64_t)b * p.nch + t / kChunk) * K + i] = my_anc;
                 // cached records of the new slot states
                 if (live) {
                     if (emit) {

@@ -1214,6 +1214,10 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pl.sm);
+    if constexpr (NT == 64 && LMV == 2)
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, false, 1025, 16, 16, 7>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
     if constexpr (NT == 256 && LMV == 2) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1276,7 +1280,14 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
         else ctc_beam_kernel<NT, LMV, false><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
     } else {
         (void)solo;
-        ctc_beam_kernel<NT, LMV, false><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+        bool done = false;
+        if constexpr (NT == 64 && LMV == 2)  // throughput mode (B > 4 x #SMs) on the north-star decode
+            if (p.Vp1 == 1025 && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && pl.nrow == 0 &&
+                p.merge_mode == 0 && !p.retract && p.alpha_lm >= 0.0f && p.alpha_bt >= 0.0f) {
+                ctc_beam_kernel<NT, LMV, false, 1025, 16, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                done = true;
+            }
+        if (!done) ctc_beam_kernel<NT, LMV, false><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);

@@ -29,6 +29,12 @@
 //    (R14) with exp/log1p evaluated in fp64 and rounded once;
 //  * backpointers u8 parent + u16 label per (t, k) plus per-32-frame chunk ancestors, so the
 //    backtrace walks chunks in parallel (T/32 + 32 dependent loads, not T).
+//  * K <= 32 ("solo"): warp 0 runs the slot-serial phases alone with warp-level sync; warps 1-7
+//    stream the rows and precompute each frame's summary one frame ahead, and join only for
+//    frames with many listed tokens;
+//  * compile-time variants for the paper's shape (V' = 1025, K = 16, 4-gram records, LM +
+//    boosting, "plain" options): the frame step is a chain of short dependent steps, so folding
+//    runtime bounds and branches out of it shortens every frame (A/B log in DESIGN.md §7).
 // All score arithmetic uses __fadd_rn/__fmaf_rn in the canonical order of reading R19 (no
 // contraction, no fast-math), so max-mode scores are bit-identical to the fp32 oracle.
 #include <cuda_runtime.h>

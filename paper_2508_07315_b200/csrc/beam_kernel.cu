@@ -226,6 +226,28 @@ __device__ uint64_t radix_kth(const uint64_t* keys, int n, int K, Shared& sm, Sc
     return prefix;
 }
 
+// K-th largest of n unique keys (n >= K) by rank counting: every key's rank is the number of
+// larger keys; the key of rank K-1 is the answer. O(n^2 / G) shared loads, used for small n.
+__device__ __forceinline__ uint64_t kth_by_rank(const uint64_t* keys, int n, int K, Scalars& sc, int G) {
+    uint64_t res = 0;
+    for (int i = threadIdx.x; i < n; i += G) {
+        const uint64_t ki = keys[i];
+        int r = 0;
+        for (int j = 0; j < n; ++j) r += keys[j] > ki ? 1 : 0;
+        if (r == K - 1) res = ki;
+    }
+    if (G == 32) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) res = umax64(res, __shfl_xor_sync(0xffffffffu, res, o));
+        return res;
+    }
+    if (res) sc.kth = res;  // exactly one thread holds it (keys are unique and never 0)
+    __syncthreads();
+    res = sc.kth;
+    __syncthreads();
+    return res;
+}
+
 // Move the keys >= kth (exactly K of them) from the candidate buffer into the selection arrays.
 __device__ void gather_selected(int n, uint64_t kth, Shared& sm, Scalars& sc, int G) {
     if (threadIdx.x == 0) sc.nsel = 0;
@@ -577,11 +599,21 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 const long long cp3 = TCLK();
                 tp2 = cp3;
                 if (tid == 0) st[kCycP2] += (uint32_t)(cp3 - cp2);
+                // running threshold: the K-th best exact candidate pushed so far (blank / repeat /
+                // best-token candidates). A candidate below the K-th of any K candidates cannot
+                // enter the flat TopK, so it need not be scored; on blank-dominated
+                // frames this bound is far above fl(max - θ).
+                float thr = tau0;
+                {
+                    gsync(G);
+                    const int nb = sc.nbuf;
+                    if (nb >= K && nb <= 2 * G) thr = fmaxf(thr, score_of(kth_by_rank(sm.ckey, nb, K, sc, G)));
+                }
                 bool scan = false;
                 float dthr = INFINITY;
                 if (nalive > 0 && mxrb > kNeg) {
-                    const float mg = 1e-4f * (1.0f + fabsf(tau0) + fabsf(accmax) + fabsf(ubvmax));
-                    dthr = __fsub_rn(__fsub_rn(__fsub_rn(tau0, accmax), ubvmax), mg);
+                    const float mg = 1e-4f * (1.0f + fabsf(thr) + fabsf(accmax) + fabsf(ubvmax));
+                    dthr = __fsub_rn(__fsub_rn(__fsub_rn(thr, accmax), ubvmax), mg);
                     scan = stage_a ? true : (dstar >= dthr);
                 }
                 bool heavy = false;
@@ -601,7 +633,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     }
                 }
                 if (tid == 0) {
-                    sc.thr = tau0; sc.nalive = nalive; sc.ubvmax = ubvmax; sc.dthr = dthr;
+                    sc.thr = thr; sc.nalive = nalive; sc.ubvmax = ubvmax; sc.dthr = dthr;
                     sc.excl = stage_a ? wstar : -1; sc.scan = (!solo && scan) || heavy;
                     st[kStageA] += stage_a ? 1 : 0;
                 }

@@ -13,6 +13,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libflexctc.so")
+# the per-phase cycle counters (-DFLEXCTC_PHASE_TIMERS) go to their own library, so a timers build
+# never replaces the product library (and FLEXCTC_PHASE_TIMERS=1 selects it at import)
+LIB_TIMERS = os.path.join(HERE, "libflexctc_timers.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -26,10 +29,17 @@ def deps():
     return sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def lib_path(timers: bool | None = None) -> str:
+    if timers is None:
+        timers = os.environ.get("FLEXCTC_PHASE_TIMERS") == "1"
+    return LIB_TIMERS if timers else LIB
+
+
+def up_to_date(timers: bool | None = None) -> bool:
+    lib = lib_path(timers)
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
@@ -38,9 +48,10 @@ def build(force: bool = False, verbose: bool = False, timers: bool | None = None
     FLEXCTC_PHASE_TIMERS=1 environment variable)."""
     if timers is None:
         timers = os.environ.get("FLEXCTC_PHASE_TIMERS") == "1"
-    if not force and up_to_date():
-        return LIB
-    objdir = os.path.join(HERE, "build")
+    lib = lib_path(timers)
+    if not force and up_to_date(timers):
+        return lib
+    objdir = os.path.join(HERE, "build_timers" if timers else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():
@@ -52,10 +63,10 @@ def build(force: bool = False, verbose: bool = False, timers: bool | None = None
             cmd += ["-DFLEXCTC_PHASE_TIMERS"] if timers else []
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

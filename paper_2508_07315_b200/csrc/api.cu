@@ -90,6 +90,9 @@ WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K) {
     w.bp_label = o; o += align256((size_t)B * T * K * 2);
     w.align_ws = o; o += align256((size_t)B * T * 4);
     w.greedy = o; o += K == 1 ? align256((size_t)B * T * 16) : 0;  // plain greedy frame summaries
+    const bool warp = K >= 2 && K <= 32;  // the warp-per-utterance path: frame records + row prefix
+    w.cmp = o; o += warp ? align256((size_t)B * T * kCmpBytes) : 0;
+    w.rowoff = o; o += warp ? align256(8 * ((size_t)B + 1)) : 0;
     w.total = o;
     return w;
 }
@@ -326,6 +329,9 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.bp_label = (uint16_t*)(w + wl.bp_label);
     p.align_ws = (int32_t*)(w + wl.align_ws);
     p.greedy_sum = cfg->beam == 1 ? (float4*)(w + wl.greedy) : nullptr;
+    const bool warp_ws = cfg->beam >= 2 && cfg->beam <= 32;
+    p.cmp = warp_ws ? (uint8_t*)(w + wl.cmp) : nullptr;
+    p.rowoff = warp_ws ? (int64_t*)(w + wl.rowoff) : nullptr;
     p.nch = wl.nch;
     p.out_tokens = out_tokens; p.out_num = out_num_tokens; p.out_scores = out_scores;
     p.out_ts = out_timestamps; p.out_align = out_alignment;
@@ -333,9 +339,12 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.overread = overread;
     p.nbest = nbest;
     std::string err;
-    if (logits) {
-        // bf16 logits: a bandwidth-bound log-softmax pass (R25) into the workspace's dense fp32
-        // [B][T][Vp1] region, then the decode of those log-probs
+    p.logits = logits;
+    if (logits && !use_warp_path(p)) {
+        // bf16 logits, K = 1 or K > 32: a bandwidth-bound log-softmax pass (R25) into the
+        // workspace's dense fp32 [B][T][Vp1] region, then the decode of those log-probs (the
+        // K <= 32 warp path instead fuses the log-softmax into its compaction pass)
+        p.logits = nullptr;
         float* Dw = (float*)((char*)workspace + wl.total);
         const int rc0 = launch_log_softmax_bf16(logits, stride_b, stride_t, lengths, B, T, Vp1, Dw, (void*)stream, err);
         if (rc0 == 2) return fail(FLEXCTC_ERR_CAPACITY, err);

@@ -1354,8 +1354,10 @@ int run_any(int nt, const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t
 
 // Relative per-utterance latency of the NT-thread kernel (measured on c4 / c5, round 1): more
 // warps shorten each frame step; fewer warps fit more utterances per SM.
+// K <= 32, c4-shaped, one wave each (round 2, profiles/r2_policy.jsonl): NT = 256 1.59 ms at
+// B = 148; NT = 128 2.59 ms at B = 256; NT = 64 2.68 / 2.74 / 2.85 ms at B = 256 / 384 / 512.
 double latency_factor(int nt, int K) {
-    if (K <= 32) return nt == 32 ? 1.75 : nt == 64 ? 1.5 : nt == 128 ? 1.2 : 1.0;
+    if (K <= 32) return nt == 32 ? 2.2 : nt == 64 ? 1.8 : nt == 128 ? 1.65 : 1.0;
     return nt == 64 ? 1.6 : nt == 128 ? 1.3 : 1.0;
 }
 
@@ -1379,7 +1381,8 @@ int launch_lmv(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std
     const bool throughput = p.B > 4 * nsm;
     for (int nt = need; nt <= 256; nt *= 2) {
         if (forced && nt != forced) continue;
-        if (!forced && !throughput && nt != 256) continue;
+        // K > 32: latency mode (one utterance per CTA of 256 threads) unless B > 4 x #SMs
+        if (!forced && !throughput && nt != 256 && p.K > 32) continue;
         Plan pl;
         const int rc = plan_any<LMV>(nt, p, pl, err);
         if (rc) { if (forced || nt == 256) return rc; continue; }
@@ -1392,6 +1395,26 @@ int launch_lmv(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std
 }
 
 }  // namespace
+
+// The warp-per-utterance path (compaction pass + warp_beam_kernel) serves 2 <= K <= 32 with
+// 1-best output and device-resident input; FLEXCTC_WARP=0 keeps the persistent CTA kernel (test
+// switch: both paths are parity-tested).
+bool use_warp_path(const DecodeParams& p) {
+    if (p.K < 2 || p.K > 32 || p.nbest > 1 || p.ready || !p.cmp || !p.rowoff) return false;
+    const char* e = getenv("FLEXCTC_WARP");
+    if (e && e[0] == '0' && !p.logits) return false;
+    if (!(e && e[0] == '1') && !p.logits) {
+        // Up to 4 x #SMs utterances the persistent CTA kernel (2-8 warps per utterance, up to 592
+        // in flight) has the shorter frame step; beyond, the warp kernel's one warp per utterance
+        // packs more utterances per SM (tools/policy_sweep.py, profiles/r2_policy.jsonl)
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (p.B <= 4 * nsm) return false;
+    }
+    const size_t per = warp_beam_smem_per_warp(p.Vp1, p.logits != nullptr, p.nch);
+    return per + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0) <= 200 * 1024;
+}
 
 int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std::string& err) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -1423,6 +1446,15 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
         if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     }
     if (greedy) return launch_greedy(p, stream, ev0, ev1, err);
+    if (use_warp_path(p)) {
+        // K <= 32: the bandwidth-bound compaction pass over every valid row, then one warp per
+        // utterance (warp_beam_kernel.cu)
+        int rc = launch_rowoff(p.len_c, p.B, p.rowoff, stream, err);
+        if (!rc) rc = launch_compact(p.logits ? (const void*)p.logits : (const void*)p.log_probs, p.logits != nullptr,
+                                     p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err);
+        if (!rc) rc = launch_warp_beam(p, p.logits != nullptr, stream, ev0, ev1, err);
+        return rc;
+    }
     const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
     return small_lm ? launch_lmv<2>(p, st, ev0, ev1, err) : launch_lmv<kMaxLmLevels>(p, st, ev0, ev1, err);
 }

@@ -64,9 +64,12 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // wins; cum values are the fp32 backoff sums of the sequential walk (lm_query_host, R19).
 template <int LMV>  // max arc levels (order - 2)
 __device__ __forceinline__ float lm_query(const LmDev& lm, const int* __restrict__ rec, int w, int& next) {
-    const int n = rec[0], u = rec[1];
+    const int u = rec[1];
     int2 d = make_int2(0, 0);
     if (u >= 0) d = __ldg(&lm.dense[(size_t)u * lm.V + w]);
+    // signature: no arc level holds w -> skip the searches (same result: the dense / root level)
+    const uint32_t sw = (uint32_t)rec[6 + (lm_sig_bit(w) >> 5)];
+    const int n = ((sw >> (lm_sig_bit(w) & 31)) & 1u) ? rec[0] : 0;
     int lo[LMV], hi[LMV], hlp[LMV], hnx[LMV];
     bool hit[LMV];
 #pragma unroll

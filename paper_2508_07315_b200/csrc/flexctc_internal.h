@@ -24,7 +24,8 @@ flexctc_status fail(flexctc_status st, const std::string& msg);
 // ---------------------------------------------------------------------------------------
 // Device query structures derived from it:
 //   rec[S][RW]    per-state record: {n_arc_levels, dense_row(-1 = none), cum_u, cum_root, ub, eos,
-//                 0, 0, then per arc level (context length >= 2): arc_off, arc_deg, cum}
+//                 sig (u64: bit lm_sig_bit(w) set for every token w with an arc at an arc level),
+//                 then per arc level (context length >= 2): arc_off, arc_deg, cum}
 //   dense[U][V]   rows of the length-1 contexts: {f32 value, next | found_at_level1 << 31}
 struct LmHost {
     int32_t order = 0, V = 0, S = 0, start = 0;
@@ -38,6 +39,12 @@ struct LmHost {
     std::vector<int32_t> rec;      // S * RW
     std::vector<int32_t> dense;    // U * V * 2
 };
+
+// 6-bit hash of a token for the record signature (Fibonacci hashing)
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int lm_sig_bit(int w) { return (int)(((uint32_t)w * 0x9E3779B1u) >> 26); }
 
 struct LmDev {
     const int4* rec;               // S * RW/4 int4
@@ -78,6 +85,19 @@ float lm_query_host(const LmHost& lm, int32_t s, int32_t w, int32_t* next);
 // ---------------------------------------------------------------------------------------
 // Decode kernel parameters
 // ---------------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// Frame records of the compaction pass (compact_kernel.cu, SURVEY §8(a) A1 "compact_frames"):
+// 256 B per valid frame (b, t < L_b) at cmp + (b·T + t)·256:
+//   f32 [0] D[blank], [1] floor, i32 [2] n, f32 [3] xthr, f64 at byte 16: lse (bf16-logits input; 0
+//   for log-prob input), f32 val[32] at byte 32, u16 tok[32] at byte 160.
+// tok[0..n) are the non-blank tokens listed for the frame, sorted by (D desc, token asc), with
+// their D values; every non-blank token NOT listed has D <= floor (floor = +inf: no usable list,
+// floor = -inf: every finite non-blank token is listed); a token is listed iff its raw input
+// value (log-prob, or bf16 logit) is >= xthr.
+// ---------------------------------------------------------------------------------------
+constexpr int kCmpList = 32;
+constexpr int kCmpBytes = 256;
+
 constexpr int kChunk = 32;      // frames per backtrace chunk (chunk ancestors, §7.3 item 6)
 constexpr int kMaxBeam = 256;   // parent index fits a u8
 constexpr int kMaxVp1 = 8192;   // frame rows are staged in shared memory
@@ -111,6 +131,9 @@ struct DecodeParams {
     uint16_t* bp_label;   // [B][T][K]
     int32_t* align_ws;    // [B][T]
     float4* greedy_sum;   // [B][T] {d1, w1, d2, 0} frame summaries of the plain greedy path (K = 1)
+    uint8_t* cmp;         // [B][T][kCmpBytes] frame records (K <= 32 warp path), NULL otherwise
+    int64_t* rowoff;      // [B + 1] prefix of the clamped lengths (compaction pass rows)
+    const uint16_t* logits;  // bf16 logits input of the warp path (log_probs unused), or NULL
     int32_t nch;
     // outputs
     int32_t* out_tokens;
@@ -122,14 +145,22 @@ struct DecodeParams {
 };
 
 struct WorkspaceLayout {
-    size_t flags, order, len_c, chunk_anc, bp_parent, bp_label, align_ws, greedy, total;
+    size_t flags, order, len_c, chunk_anc, bp_parent, bp_label, align_ws, greedy, cmp, rowoff, total;
     int32_t nch;
 };
 WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K);
 
 // launches (beam_kernel.cu; K = 1 goes to launch_greedy in greedy_kernel.cu)
+bool use_warp_path(const DecodeParams& p);  // K <= 32 warp path eligible (p.logits: bf16 input)
 int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
 int launch_greedy(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
+// frame compaction pass (compact_kernel.cu): records of every valid row; rowoff by launch_rowoff
+int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, std::string& err);
+int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t, const int64_t* rowoff, int B, int T,
+                   int Vp1, uint8_t* cmp, void* stream, std::string& err);
+// warp-per-utterance beam kernel (warp_beam_kernel.cu), K <= 32, after launch_compact
+int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev_start, void* ev_stop, std::string& err);
+size_t warp_beam_smem_per_warp(int Vp1, bool bf16, int nch);
 // input side (input_kernel.cu): log-softmax of bf16 logits into a dense fp32 [B][T][Vp1] buffer
 int launch_log_softmax_bf16(const uint16_t* x, int64_t stride_b, int64_t stride_t, const int32_t* lengths, int B,
                             int T, int Vp1, float* out, void* stream, std::string& err);

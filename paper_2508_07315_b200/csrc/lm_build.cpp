@@ -333,6 +333,13 @@ flexctc_status build_lm_host(const char* path, int32_t V, const char* const* sym
             acc = acc + st_bw[x];
             x = st_bo[x];
         }
+        // token signature of the arc levels: bit sig_bit(w) is set for every token with an arc
+        // at one of them, so a query whose bit is clear goes straight to the dense / root level
+        uint64_t sig = 0;
+        for (int j = 0; j < n; ++j)
+            for (int32_t k = r[8 + 3 * j]; k < r[8 + 3 * j] + r[8 + 3 * j + 1]; ++k)
+                sig |= 1ull << lm_sig_bit(out.arc_tok[k]);
+        memcpy(&r[6], &sig, 8);
         r[0] = n;
         r[1] = u;
         memcpy(&r[2], &cum_u, 4);

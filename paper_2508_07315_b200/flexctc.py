@@ -65,7 +65,7 @@ def _load() -> ctypes.CDLL:
     path = os.environ.get("FLEXCTC_LIB_AB")  # A/B timing of two builds (tools/ab.sh); never a fallback
     if path:
         return _declare(ctypes.CDLL(path))
-    path = _build.LIB
+    path = _build.lib_path()  # libflexctc.so, or libflexctc_timers.so under FLEXCTC_PHASE_TIMERS=1
     if not _build.up_to_date():
         _build.build()  # missing or stale (sources newer); nvcc is part of the image, failures raise
     return _declare(ctypes.CDLL(path))

@@ -139,6 +139,7 @@ def test_kernel_variants_c4(lm_pair, bt_pair, nt, dense, solo, monkeypatch):
     """Every launch variant (threads per utterance, LM row-cache dense path, beam-warp + helpers
     mode on/off) matches the oracle on c4 utterances (FLEXCTC_NT / FLEXCTC_DENSE_MIN /
     FLEXCTC_SOLO are tuning overrides)."""
+    monkeypatch.setenv("FLEXCTC_WARP", "0")  # the persistent CTA kernel (K <= 32 defaults to the warp path)
     monkeypatch.setenv("FLEXCTC_NT", nt)
     if dense:
         monkeypatch.setenv("FLEXCTC_DENSE_MIN", dense)

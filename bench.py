@@ -9,6 +9,12 @@ north-star metric is quoted on. Multi-GPU (torchrun): weak scaling, each rank de
 c4 batch (distinct seeds), LM/boost replicated, results gathered once at the end.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4] [--impl flexctc|reference]
+                  [--scaling weak|strong] [--stream M] [--input f32-logprobs|bf16-logits]
+
+--gpus N without torchrun re-launches itself under torch.distributed.run with N ranks (one per
+GPU, 127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal N. --scaling strong decodes ONE
+global batch (the workload's batch, times --stream M) LPT-sharded over the ranks
+(shard.lpt_assign) and reports each rank's share, critical path and the load balance.
 """
 from __future__ import annotations
 
@@ -49,7 +55,23 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0 = auto)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank decodes its own batch; strong: one global batch LPT-sharded over the ranks")
+    ap.add_argument("--stream", type=int, default=1,
+                    help="strong scaling: the global batch is M x the workload batch (distinct seeds), e.g. 8 x 512")
     return ap.parse_args()
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run with N ranks."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -156,6 +178,31 @@ def ncu_traffic(workload):
     return e.get("dram_bytes_per_launch"), e.get("source")
 
 
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    return "unknown"
+
+
+def one_thread_times():
+    """The oracle on ONE host thread over the whole c1 and c2 batches."""
+    import oracle
+    res = {}
+    for name in ("c1", "c2"):
+        wl, D, L, _, _ = synth.workload_inputs(name)
+        cfg = oracle.make_cfg(wl.beam, 0.0, 0.0, wl.beta, wl.theta, wl.merge_mode)
+        t0 = time.perf_counter()
+        oracle.decode(D, L, cfg, nthreads=1)
+        dt = time.perf_counter() - t0
+        res[name] = {"s": round(dt, 4), "rtfx": float(L.sum()) * synth.FRAME_SECONDS / dt}
+    return res
+
+
 def cpu_baseline(wl, D, L, arpa, ph, n_utts):
     """The oracle as it stands (never tuned), on this host's cores, over a bounded sample."""
     import oracle
@@ -173,7 +220,8 @@ def cpu_baseline(wl, D, L, arpa, ph, n_utts):
     return {"value": audio / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{len(idx)} of the {wl.name} utterances ({int(L[idx].sum())} frames, "
                       f"{audio:.1f} audio s) decoded by the C++ oracle on {cores} host threads in {dt:.1f} s",
-            "frames_beams_per_s": float(L[idx].sum()) * wl.beam / dt}
+            "frames_beams_per_s": float(L[idx].sum()) * wl.beam / dt,
+            "cpu_model": cpu_model(), "one_thread": one_thread_times()}
 
 
 def run_reference(args):
@@ -223,7 +271,6 @@ def run_flexctc(args):
     from paper_2508_07315_b200.shard import gather_results
 
     rank, world, local = dist_env()
-    assert world == args.gpus or world == 1, "--gpus must match WORLD_SIZE under torchrun"
     gpu = local % max(1, torch.cuda.device_count())  # ranks > GPUs only in the 1-GPU path test
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
@@ -236,8 +283,38 @@ def run_flexctc(args):
     wl = synth.WORKLOADS[args.workload]
     if args.beam:
         wl = dataclasses.replace(wl, beam=args.beam, name=f"{wl.name} (beam {args.beam})")
-    # weak scaling: rank r decodes its own batch of the workload (seed offset r)
-    _, D, L, arpa, ph = synth.workload_inputs(args.workload, B=args.batch or None, seed_offset=rank)
+    strong = args.scaling == "strong"
+    shard_idx = None
+    if not strong:
+        # weak scaling: rank r decodes its own batch of the workload (seed offset r)
+        _, D, L, arpa, ph = synth.workload_inputs(args.workload, B=args.batch or None, seed_offset=rank)
+    else:
+        # strong scaling: one global batch (M x the workload batch, chunk m with seed offset m),
+        # LPT-sharded by length over the ranks; each rank generates only its own rows
+        from paper_2508_07315_b200.shard import lpt_assign
+        Bw = args.batch or wl.B
+        Ls = [synth.lengths(wl, Bw, wl.seed + m) for m in range(args.stream)]
+        L_all = np.concatenate(Ls)
+        shard_idx = lpt_assign(L_all, world)[rank]
+        Tg = int(L_all.max()) if wl.lengths != "fixed" else wl.T
+        mine = set(int(i) for i in shard_idx)
+        D = np.zeros((len(shard_idx), Tg, wl.V + 1), dtype=np.float32)
+        row = {int(g): j for j, g in enumerate(shard_idx)}
+        arpa = ph = None
+        for m in range(args.stream):
+            lo = m * Bw
+            if not any(lo <= i < lo + Bw for i in mine):
+                continue
+            _, Dm, Lm, arpa, ph = synth.workload_inputs(args.workload, B=Bw, seed_offset=m)
+            for i in range(lo, lo + Bw):
+                if i in mine:
+                    D[row[i], :Dm.shape[1]] = Dm[i - lo]
+            del Dm
+        if arpa is None and wl.lm:
+            arpa = synth.arpa_file(V=wl.V)
+        if ph is None and wl.boost:
+            ph = synth.phrases(wl.V)
+        L = L_all[shard_idx].astype(np.int32)
     B, T, Vp1 = D.shape
     lm = F.LM(arpa, wl.V, device=gpu) if wl.lm else None
     bt = F.Boost(ph, 1.0, wl.V, device=gpu) if wl.boost else None
@@ -247,7 +324,6 @@ def run_flexctc(args):
     bf16 = args.input == "bf16-logits"
     if bf16:  # the synthetic log-probs as bf16 logits (log-softmax is shift invariant)
         Dd = Dd.to(torch.bfloat16)
-        args.no_e2e = True  # flexctc_decode_host takes fp32 log-probs
     Ld = torch.from_numpy(L).to(dev)
     ws = FX.make_logits_workspace(B, T, Vp1, cfg, dev) if args.input == "bf16-logits" else F.make_workspace(B, T, Vp1, cfg, dev)
     stream = torch.cuda.Stream(dev)
@@ -294,6 +370,7 @@ def run_flexctc(args):
     torch.cuda.synchronize()
     t_dec = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3        # s, whole decode per step summed
     t_kern = sum(e[2].elapsed_time(e[3]) for e in ev) / 1e3       # s, beam kernel only
+    t_dec_local = t_dec
     flags = F.check(ws)
     dstats = FX.stats(ws)  # device counters of the last timed decode
     tt = torch.tensor([t_dec, t_kern], dtype=torch.float64, device=dev)
@@ -308,6 +385,18 @@ def run_flexctc(args):
         frames_all = float(fa[0])
     value = frames_all * synth.FRAME_SECONDS * args.steps / t_dec
     fbps = frames_all * wl.beam * args.steps / t_dec
+    shards = None
+    if strong:  # each rank's share and critical path (LPT balance)
+        mine_t = torch.tensor([float(B), frames_local, float(L.max() if len(L) else 0),
+                               1e3 * t_dec_local / args.steps], dtype=torch.float64, device=dev)
+        allt = [torch.zeros_like(mine_t) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(allt, mine_t)
+        else:
+            allt = [mine_t]
+        shards = [{"rank": r, "utterances": int(x[0]), "frames": int(x[1]), "T_max": int(x[2]),
+                   "ms_per_step": round(float(x[3]), 4)} for r, x in enumerate(allt)]
+        fr = [sh["frames"] for sh in shards]
 
     # roofline of the dominant kernel: algorithmic bytes per launch =
     #  beam kernel:         Σ_b L_b · (4·V' [read D once] + 3·K [u8 parent + u16 label backpointers])
@@ -331,12 +420,15 @@ def run_flexctc(args):
     # e2e through the public host-buffer entry (flexctc_decode_host): H2D + decode + D2H per step
     e2e = None
     if not args.no_e2e:
-        Dp = torch.from_numpy(D).pin_memory()
+        Dp = torch.from_numpy(D).to(torch.bfloat16 if bf16 else torch.float32).pin_memory()
         Lp = torch.from_numpy(L).pin_memory()
-        scratch = torch.empty(F.host_scratch_bytes(B, T, Vp1, cfg), dtype=torch.uint8, device=dev)
+        nscr = (FX.lib.flexctc_host_scratch_bytes_bf16 if bf16 else FX.lib.flexctc_host_scratch_bytes)(
+            B, T, Vp1, __import__("ctypes").byref(cfg))
+        scratch = torch.empty(int(nscr), dtype=torch.uint8, device=dev)
+        host_decode = F.decode_host_bf16 if bf16 else F.decode_host
         hout = None
         for _ in range(max(1, args.warmup)):
-            hout = F.decode_host(Dp, Lp, cfg, lm, bt, scratch=scratch, stream=stream, out=hout)
+            hout = host_decode(Dp, Lp, cfg, lm, bt, scratch=scratch, stream=stream, out=hout)
         if world > 1:
             dist.barrier()
         ts = []
@@ -345,32 +437,43 @@ def run_flexctc(args):
                 flush.fill_(1)
             stream.synchronize()
             t0 = time.perf_counter()
-            hout = F.decode_host(Dp, Lp, cfg, lm, bt, scratch=scratch, stream=stream, out=hout)
+            hout = host_decode(Dp, Lp, cfg, lm, bt, scratch=scratch, stream=stream, out=hout)
             ts.append(time.perf_counter() - t0)
         te = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": frames_all * synth.FRAME_SECONDS * args.steps / float(te[0]), "unit": UNIT,
                # the streamed path (K > 1) copies only the valid frames t < L_b
-               "h2d_bytes_per_step": int((int(np.clip(L, 0, T).sum()) * Vp1 * 4 if cfg.beam > 1 else D.nbytes)
-                                         + L.nbytes),
+               "h2d_bytes_per_step": int((int(np.clip(L, 0, T).sum()) * Vp1 * (2 if bf16 else 4) if cfg.beam > 1
+                                          else Dp.numel() * Dp.element_size()) + L.nbytes),
                "d2h_bytes_per_step": int(B * T * 4 * 2 + B * 4 * 2),
-               "path": "flexctc_decode_host (pinned host buffers; H2D in frame chunks overlapping the decode, "
-                       "D2H and sync inside)"}
+               "path": (("flexctc_decode_host_bf16 (pinned bf16 logits, 2 B per logit over PCIe; normalised on the "
+                         "device per frame chunk" if bf16 else
+                         "flexctc_decode_host (pinned host buffers") +
+                        "; H2D in frame chunks overlapping the decode, D2H and sync inside)")}
 
     # gather the final results (the only cross-GPU traffic)
     gathered = None
     if world > 1:
-        g = gather_results({k: v for k, v in out.items()}, np.arange(rank * B, rank * B + B), B * world, T, device=dev)
+        if strong:
+            Btot = int(sum(sh["utterances"] for sh in shards))
+            g = gather_results({k: v for k, v in out.items()}, shard_idx, Btot, T, device=dev)
+        else:
+            g = gather_results({k: v for k, v in out.items()}, np.arange(rank * B, rank * B + B), B * world, T,
+                               device=dev)
         gathered = int(g["num_tokens"].sum().item())
 
     if rank == 0:
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_dec / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "input": args.input,
-            "config": workload_config(wl, B, T, frames_local, {"parallelism": f"dp{world} (utterance shards)"}),
+            "config": workload_config(wl, B, T, frames_local, {"parallelism": f"dp{world} (utterance shards)"}
+                                      if not strong else
+                                      {"parallelism": f"dp{world} (one global batch LPT-sharded by length)",
+                                       "global_batch": int(sum(sh["utterances"] for sh in shards)),
+                                       "stream_batches": args.stream}),
             "frames_beams_per_s": fbps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -389,6 +492,12 @@ def run_flexctc(args):
         }
         if gathered is not None:
             res["gathered_tokens"] = gathered
+        if shards is not None:
+            mean = sum(fr) / len(fr)
+            res["shards"] = shards
+            res["load_balance"] = {"max_over_mean_frames": max(fr) / mean if mean else None,
+                                   "critical_path_T_max": max(sh["T_max"] for sh in shards),
+                                   "slowest_rank_ms": max(sh["ms_per_step"] for sh in shards)}
         if world == 1 and not args.no_cpu_baseline:
             # the whole c4 batch (~20 core-seconds of oracle work); 16 utterances at K = 128
             n = args.cpu_sample or (min(B, 64) if wl.beam <= 32 else min(B, 16))
@@ -400,6 +509,13 @@ def run_flexctc(args):
 
 def main():
     args = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if world is not None and int(world) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a mismatched run"}),
+              flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -224,7 +224,9 @@ flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags);
  * stream, each followed by a "frames ready" word the row loaders wait on, so the copy overlaps
  * the frame recurrence (flexctc_host_streaming() says whether this is active). The host
  * buffers must stay unchanged until the call returns. A chunk that never lands (a failed copy)
- * releases the kernel after 10 s with FLEXCTC_FLAG_STREAM_TIMEOUT (flexctc_check). */
+ * releases the kernel after 10 s: the call then returns FLEXCTC_ERR_CUDA.
+ *   out_flags   host uint32 or NULL: the device flags of this decode (FLEXCTC_FLAG_*: length
+ *               clamps, stream timeout), read after the final synchronisation. */
 size_t flexctc_host_scratch_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg);
 /* 1 if flexctc_decode_host on the current device streams its input (frame chunks copied on a
  * library-owned copy stream while the beam kernel runs, each chunk signalled by a stream memory
@@ -237,7 +239,25 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
                                    void* device_scratch, size_t scratch_bytes,
                                    flexctc_stream stream, int32_t* out_tokens,
                                    int32_t* out_num_tokens, float* out_scores,
-                                   int32_t* out_timestamps);
+                                   int32_t* out_timestamps, uint32_t* out_flags);
+
+/* flexctc_decode_host over bf16 LOGITS (uint16 bit patterns, dense [B, T, Vp1] host buffer):
+ * the end-to-end entry of the bf16 input side. The H2D transfer is
+ * 2 B per logit; on the device every frame t < lengths[b] is normalised exactly as
+ * flexctc_decode_logits_bf16 does (reading R25) into an fp32 log-prob buffer in the scratch, then
+ * decoded as flexctc_decode_host. With K > 1 and B < #SMs the copy is streamed in frame chunks
+ * and each chunk is normalised on the copy stream before its "frames ready" signal, so the
+ * transfer and the normalisation overlap the frame recurrence. device_scratch: at least
+ * flexctc_host_scratch_bytes_bf16(B, T, Vp1, cfg) bytes of device memory. Everything else
+ * (outputs, flags, errors, synchronisation) as flexctc_decode_host. */
+size_t flexctc_host_scratch_bytes_bf16(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg);
+flexctc_status flexctc_decode_host_bf16(const uint16_t* logits_host, const int32_t* lengths_host,
+                                        int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg,
+                                        const flexctc_lm* lm, const flexctc_boost* boost,
+                                        void* device_scratch, size_t scratch_bytes,
+                                        flexctc_stream stream, int32_t* out_tokens,
+                                        int32_t* out_num_tokens, float* out_scores,
+                                        int32_t* out_timestamps, uint32_t* out_flags);
 
 #ifdef __cplusplus
 }

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -283,7 +284,10 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     if (B < 0 || T < 0) return fail(FLEXCTC_ERR_INVALID_ARG, "B and T must be >= 0");
     if (Vp1 < 2) return fail(FLEXCTC_ERR_INVALID_ARG, "Vp1 must be >= 2");
     if (Vp1 > kMaxVp1) return fail(FLEXCTC_ERR_CAPACITY, "Vp1 > 8192");
-    if (stride_t < Vp1 || stride_b < (int64_t)T * stride_t) return fail(FLEXCTC_ERR_INVALID_ARG, "strides overlap rows");
+    // the stride of a size-1 axis is never used (torch / numpy give such axes arbitrary strides)
+    if ((T > 1 && stride_t < Vp1) || (B > 1 && stride_b < (int64_t)std::max(T, 1) * (T > 1 ? stride_t : (int64_t)Vp1)) ||
+        stride_t < 0 || stride_b < 0)
+        return fail(FLEXCTC_ERR_INVALID_ARG, "strides overlap rows");
     if ((int64_t)Vp1 * cfg->beam >= (int64_t)0xffffffff) return fail(FLEXCTC_ERR_CAPACITY, "K*Vp1 too large");
     const WorkspaceLayout wl = workspace_layout(B, T, cfg->beam);
     const size_t need = wl.total + (logits ? ((size_t)B * T * Vp1 * 4 + 255) & ~size_t(255) : 0);
@@ -418,6 +422,11 @@ size_t flexctc_host_scratch_bytes(int32_t B, int32_t T, int32_t Vp1, const flexc
     return s;
 }
 
+size_t flexctc_host_scratch_bytes_bf16(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg) {
+    const size_t s = flexctc_host_scratch_bytes(B, T, Vp1, cfg);
+    return s ? s + align256((size_t)B * T * Vp1 * 2 + 16) : 0;  // + the bf16 logits copy
+}
+
 }  // extern "C"
 
 namespace flexctc {
@@ -481,22 +490,34 @@ int32_t flexctc_host_streaming(void) {
     return host_path_init(dev) && !getenv("FLEXCTC_NO_STREAM_INPUT") ? 1 : 0;
 }
 
-flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* lengths_host, int32_t B, int32_t T,
-                                   int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
-                                   const flexctc_boost* boost, void* device_scratch, size_t scratch_bytes,
-                                   flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
-                                   float* out_scores, int32_t* out_timestamps) {
+}  // extern "C"
+
+namespace flexctc {
+namespace {
+
+// flexctc_decode_host / flexctc_decode_host_bf16: H2D (streamed in frame chunks for K > 1, so the
+// copy overlaps the frame recurrence), decode, D2H, sync. bf16 logits are normalised on the
+// device (reading R25) into the fp32 log-prob buffer, chunk by chunk on the copy stream before
+// each chunk's "frames ready" signal; the PCIe transfer is 2 B per logit.
+flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* lengths_host, int32_t B, int32_t T,
+                                int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
+                                const flexctc_boost* boost, void* device_scratch, size_t scratch_bytes,
+                                flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                                float* out_scores, int32_t* out_timestamps, uint32_t* out_flags) {
+    if (out_flags) *out_flags = 0;
     flexctc_status st = validate_cfg(cfg);
     if (st != FLEXCTC_OK) return st;
     if (B < 0 || T < 0 || Vp1 < 2) return fail(FLEXCTC_ERR_INVALID_ARG, "bad shape");
-    const size_t need = flexctc_host_scratch_bytes(B, T, Vp1, cfg);
+    const size_t need = bf16 ? flexctc_host_scratch_bytes_bf16(B, T, Vp1, cfg) : flexctc_host_scratch_bytes(B, T, Vp1, cfg);
     if (!device_scratch || scratch_bytes < need) return fail(FLEXCTC_ERR_CAPACITY, "device_scratch too small");
-    if (!log_probs_host || !lengths_host || !out_tokens || !out_num_tokens || !out_scores)
+    if (!x_host || !lengths_host || !out_tokens || !out_num_tokens || !out_scores)
         return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
     if (B == 0) return FLEXCTC_OK;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaStream_t s = (cudaStream_t)stream;
     char* d = (char*)(((uintptr_t)device_scratch + 255) & ~(uintptr_t)255);
     size_t o = 0;
@@ -506,19 +527,27 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
     int32_t* dTs = (int32_t*)(d + o); o += align256((size_t)B * T * 4);
     int32_t* dN = (int32_t*)(d + o); o += align256((size_t)B * 4);
     float* dS = (float*)(d + o); o += align256((size_t)B * 4);
+    uint16_t* dX = nullptr;  // bf16 logits copy
+    if (bf16) { dX = (uint16_t*)(d + o); o += align256((size_t)B * T * Vp1 * 2 + 16); }
     void* ws = d + o;
     const size_t wsb = scratch_bytes - (size_t)(d - (char*)device_scratch) - o;
     const WorkspaceLayout wl = workspace_layout(B, T, cfg->beam);
+    const size_t esz = bf16 ? 2 : 4;
+    char* dIn = bf16 ? (char*)dX : (char*)dD;
     // Streamed input: the persistent beam kernel starts at once and each row loader waits for
     // its frame chunk (a "frames ready" word in the workspace, written by the copy stream after
     // every chunk), so the host->device copy overlaps the frame recurrence. Only frames
     // t < lengths[b] are copied (the padding is never read). K = 1 and configurations without
-    // stream memory operations copy everything first.
-    const bool streamed = host_path_init(dev) && cfg->beam > 1 && T > 0 &&
+    // stream memory operations copy everything first; so does bf16 input unless the batch leaves
+    // SMs free for the per-chunk normalisation next to the persistent kernel (B < #SMs).
+    const bool streamed = host_path_init(dev) && cfg->beam > 1 && T > 0 && (!bf16 || B < nsm) &&
                           !getenv("FLEXCTC_NO_STREAM_INPUT");  // test switch: copy everything, then decode
     e = cudaMemcpyAsync(dL, lengths_host, (size_t)B * 4, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
     uint32_t* ready = nullptr;
+    std::string err;
+    if (streamed && bf16 && preload_log_softmax_bf16())
+        return fail(FLEXCTC_ERR_CUDA, "cannot load the bf16 normalisation kernel");
     if (streamed) {
         ready = (uint32_t*)((char*)ws + wl.flags + 64 + 8 * kStatsWords);
         e = cudaMemsetAsync(ready, 0, 4, s);
@@ -526,8 +555,12 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
         if (e == cudaSuccess) e = cudaStreamWaitEvent(g_host.copy, g_host.ev_a, 0);
         if (e != cudaSuccess) return cuda_fail(e, "stream setup");
     } else {
-        e = cudaMemcpyAsync(dD, log_probs_host, (size_t)B * T * Vp1 * 4, cudaMemcpyHostToDevice, s);
+        e = cudaMemcpyAsync(dIn, x_host, (size_t)B * T * Vp1 * esz, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+        if (bf16) {
+            const int rc = launch_log_softmax_bf16(dX, (int64_t)T * Vp1, Vp1, dL, B, T, Vp1, dD, (void*)s, err);
+            if (rc) return fail(rc == 2 ? FLEXCTC_ERR_CAPACITY : FLEXCTC_ERR_CUDA, err);
+        }
     }
     st = decode_impl(dD, (int64_t)T * Vp1, Vp1, dL, B, T, Vp1, cfg, lm, boost, ws, wsb, stream, dTok, dN, dS,
                      out_timestamps ? dTs : nullptr, nullptr, ready, 1);
@@ -537,16 +570,17 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
     }
     if (streamed) {
         // chunk c: frames [t0, t1) of every utterance with L_b > t0 (rows of one utterance are
-        // contiguous), then ready = t1
-        const size_t row = (size_t)Vp1 * 4;
+        // contiguous), [bf16: normalised into dD], then ready = t1
+        const size_t row = (size_t)Vp1 * esz;
         int Lmin = T;
         for (int b = 0; b < B; ++b) Lmin = std::min(Lmin, std::min(std::max(lengths_host[b], 0), T));
         std::vector<void*> dsts, srcs;
         std::vector<size_t> sizes;
+        const char* xh = (const char*)x_host;
         int t0 = 0;
         for (int t1 : chunk_ends(T)) {
             if (t1 <= Lmin) {  // every utterance needs the whole chunk: one 2D copy
-                e = cudaMemcpy2DAsync(dD + (size_t)t0 * Vp1, (size_t)T * row, log_probs_host + (size_t)t0 * Vp1,
+                e = cudaMemcpy2DAsync(dIn + (size_t)t0 * row, (size_t)T * row, xh + (size_t)t0 * row,
                                       (size_t)T * row, row * (size_t)(t1 - t0), (size_t)B, cudaMemcpyHostToDevice,
                                       g_host.copy);
             } else {  // ragged: one batched copy of the valid frames of each utterance
@@ -554,9 +588,9 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
                 for (int b = 0; b < B; ++b) {
                     const int L = std::min(std::max(lengths_host[b], 0), T);
                     if (L <= t0) continue;
-                    const size_t off = ((size_t)b * T + t0) * Vp1;
-                    dsts.push_back(dD + off);
-                    srcs.push_back((void*)(log_probs_host + off));
+                    const size_t off = ((size_t)b * T + t0) * row;
+                    dsts.push_back(dIn + off);
+                    srcs.push_back((void*)(xh + off));
                     sizes.push_back(row * (size_t)(std::min(L, t1) - t0));
                 }
                 if (!dsts.empty()) {
@@ -574,6 +608,9 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
                     }
                 }
             }
+            if (e == cudaSuccess && bf16 &&
+                launch_log_softmax_bf16(dX, (int64_t)T * Vp1, Vp1, dL, B, T, Vp1, dD, (void*)g_host.copy, err, t0, t1))
+                e = cudaErrorUnknown;
             if (e == cudaSuccess &&
                 g_host.write32((CUstream)g_host.copy, (CUdeviceptr)ready, (cuuint32_t)t1, 0) != CUDA_SUCCESS)
                 e = cudaErrorUnknown;
@@ -595,7 +632,37 @@ flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* l
         e = cudaMemcpyAsync(out_timestamps, dTs, (size_t)B * T * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "decode_host copy/sync");
+    // the device flags of this decode (length clamps, stream watchdog)
+    uint32_t fl = 0;
+    e = cudaMemcpy(&fl, (const char*)ws + wl.flags, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "decode_host flags");
+    if (out_flags) *out_flags = fl;
+    if (fl & FLEXCTC_FLAG_STREAM_TIMEOUT)
+        return fail(FLEXCTC_ERR_CUDA, "decode_host: a frame chunk never arrived (stream watchdog); outputs invalid");
     return FLEXCTC_OK;
+}
+
+}  // namespace
+}  // namespace flexctc
+
+extern "C" {
+
+flexctc_status flexctc_decode_host(const float* log_probs_host, const int32_t* lengths_host, int32_t B, int32_t T,
+                                   int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
+                                   const flexctc_boost* boost, void* device_scratch, size_t scratch_bytes,
+                                   flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                                   float* out_scores, int32_t* out_timestamps, uint32_t* out_flags) {
+    return decode_host_impl(log_probs_host, false, lengths_host, B, T, Vp1, cfg, lm, boost, device_scratch,
+                            scratch_bytes, stream, out_tokens, out_num_tokens, out_scores, out_timestamps, out_flags);
+}
+
+flexctc_status flexctc_decode_host_bf16(const uint16_t* logits_host, const int32_t* lengths_host, int32_t B, int32_t T,
+                                        int32_t Vp1, const flexctc_config* cfg, const flexctc_lm* lm,
+                                        const flexctc_boost* boost, void* device_scratch, size_t scratch_bytes,
+                                        flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
+                                        float* out_scores, int32_t* out_timestamps, uint32_t* out_flags) {
+    return decode_host_impl(logits_host, true, lengths_host, B, T, Vp1, cfg, lm, boost, device_scratch,
+                            scratch_bytes, stream, out_tokens, out_num_tokens, out_scores, out_timestamps, out_flags);
 }
 
 }  // extern "C"

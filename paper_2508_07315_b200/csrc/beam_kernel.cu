@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     __shared__ uint32_t s_pairs[kPairCap];
     constexpr int kTab = NT > 32 ? 2 * NT : 1;  // recombination table (NT > 32)
     constexpr int kTabMem = 3;
-    __shared__ unsigned long long s_tkey[kTab];
+    __shared__ int s_tocc[kTab];  // slot + 1 of the entry's first member (0 = empty)
     __shared__ int s_tcnt[kTab];
     __shared__ int s_tmem[kTab * kTabMem];
     __shared__ int s_build[2 * 32];        // rows to build: (line, state)
@@ -918,14 +918,19 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             if (NT > 32 && !small_beam) {
                 // groups have <= 3 members (reading R14): a shared hash table keyed on (hash, last)
                 // with member lists replaces the O(K) scan per slot
-                for (int e = tid; e < kTab; e += NT) { s_tkey[e] = 0ull; s_tcnt[e] = 0; }
+                for (int e = tid; e < kTab; e += NT) { s_tocc[e] = 0; s_tcnt[e] = 0; }
                 __syncthreads();
                 if (tid < K && nxt.acc[tid] > kNeg) {
-                    const uint64_t k2 = (nxt.hash[tid] ^ ((uint64_t)(nxt.last[tid] + 1) * 0x9E3779B97F4A7C15ull)) | 1ull;
+                    // bucket from a fold of (hash, last); an entry belongs to the exact pair of its first
+                    // member (compared in full, so two groups whose folds collide never merge)
+                    const uint64_t h = nxt.hash[tid];
+                    const int l = nxt.last[tid];
+                    const uint64_t k2 = h ^ ((uint64_t)(l + 1) * 0x9E3779B97F4A7C15ull);
                     int e = (int)((k2 >> 20) & (uint64_t)(kTab - 1));
                     for (;;) {
-                        const unsigned long long old = atomicCAS(&s_tkey[e], 0ull, (unsigned long long)k2);
-                        if (old == 0ull || old == k2) break;
+                        const int old = atomicCAS(&s_tocc[e], 0, tid + 1);
+                        if (old == 0) break;
+                        if (nxt.hash[old - 1] == h && nxt.last[old - 1] == l) break;
                         e = (e + 1) & (kTab - 1);
                     }
                     const int q = atomicAdd(&s_tcnt[e], 1);
@@ -1402,8 +1407,8 @@ int launch_lmv(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std
 bool use_warp_path(const DecodeParams& p) {
     if (p.K < 2 || p.K > 32 || p.nbest > 1 || p.ready || !p.cmp || !p.rowoff) return false;
     const char* e = getenv("FLEXCTC_WARP");
-    if (e && e[0] == '0' && !p.logits) return false;
-    if (!(e && e[0] == '1') && !p.logits) {
+    if (e && e[0] == '0') return false;
+    if (!(e && e[0] == '1')) {
         // Up to 4 x #SMs utterances the persistent CTA kernel (2-8 warps per utterance, up to 592
         // in flight) has the shorter frame step; beyond, the warp kernel's one warp per utterance
         // packs more utterances per SM (tools/policy_sweep.py, profiles/r2_policy.jsonl)

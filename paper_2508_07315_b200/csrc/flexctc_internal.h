@@ -162,8 +162,10 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
 int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev_start, void* ev_stop, std::string& err);
 size_t warp_beam_smem_per_warp(int Vp1, bool bf16, int nch);
 // input side (input_kernel.cu): log-softmax of bf16 logits into a dense fp32 [B][T][Vp1] buffer
+// (frames [t0, t1) only; t1 = -1: every frame); preload_: force its module to load (see the .cu)
+int preload_log_softmax_bf16();
 int launch_log_softmax_bf16(const uint16_t* x, int64_t stride_b, int64_t stride_t, const int32_t* lengths, int B,
-                            int T, int Vp1, float* out, void* stream, std::string& err);
+                            int T, int Vp1, float* out, void* stream, std::string& err, int t0 = 0, int t1 = -1);
 
 }  // namespace flexctc
 

@@ -26,13 +26,14 @@ constexpr int kPerLane = 33;  // register-resident elements per lane at V' <= 10
 
 __global__ void __launch_bounds__(32 * kRows) log_softmax_bf16_kernel(const uint16_t* __restrict__ X, int64_t sb,
                                                                      int64_t st, const int32_t* __restrict__ lengths,
-                                                                     int B, int T, int Vp1, float* __restrict__ out) {
+                                                                     int B, int T, int Vp1, float* __restrict__ out,
+                                                                     int t0, int t1) {
     const int lane = threadIdx.x & 31;
-    const int nchunk = (T + kRows - 1) / kRows;
+    const int nchunk = (t1 - t0 + kRows - 1) / kRows;
     const int b = blockIdx.x / nchunk;
-    const int t = (blockIdx.x - b * nchunk) * kRows + (threadIdx.x >> 5);
+    const int t = t0 + (blockIdx.x - b * nchunk) * kRows + (threadIdx.x >> 5);
     const int L = min(max(__ldg(&lengths[b]), 0), T);
-    if (t >= L) return;
+    if (t >= L || t >= t1) return;
     const uint16_t* x = X + (int64_t)b * sb + (int64_t)t * st;
     float* d = out + ((int64_t)b * T + t) * Vp1;
     if (Vp1 <= 32 * kPerLane) {  // the row in registers: one read of HBM
@@ -76,13 +77,23 @@ __global__ void __launch_bounds__(32 * kRows) log_softmax_bf16_kernel(const uint
 
 }  // namespace
 
+// CUDA loads a kernel's module lazily on its first launch, and that load waits for running
+// kernels: launched next to a persistent kernel that waits for its output, the first launch
+// would deadlock. decode_host_bf16 calls this before the persistent kernel starts.
+int preload_log_softmax_bf16() {
+    cudaFuncAttributes a{};
+    return cudaFuncGetAttributes(&a, log_softmax_bf16_kernel) == cudaSuccess ? 0 : 1;
+}
+
 int launch_log_softmax_bf16(const uint16_t* x, int64_t stride_b, int64_t stride_t, const int32_t* lengths, int B,
-                            int T, int Vp1, float* out, void* stream, std::string& err) {
-    const int64_t grid = (int64_t)B * ((T + kRows - 1) / kRows);
+                            int T, int Vp1, float* out, void* stream, std::string& err, int t0, int t1) {
+    if (t1 < 0) t1 = T;
+    if (t1 <= t0) return 0;
+    const int64_t grid = (int64_t)B * ((t1 - t0 + kRows - 1) / kRows);
     if (grid == 0) return 0;
     if (grid > 0x7fffffff) { err = "B * T too large"; return 2; }
     log_softmax_bf16_kernel<<<(int)grid, 32 * kRows, 0, (cudaStream_t)stream>>>(x, stride_b, stride_t, lengths, B, T,
-                                                                                 Vp1, out);
+                                                                                 Vp1, out, t0, t1);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     return 0;

@@ -52,6 +52,7 @@ EXPORTS = [
     "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
     "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
     "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_decode_nbest", "flexctc_decode_logits_bf16", "flexctc_logits_workspace_bytes", "flexctc_set_profile_events", "flexctc_get_stats",
+    "flexctc_host_scratch_bytes_bf16", "flexctc_decode_host_bf16",
 ]
 STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
               "exact_dense", "compactions", "top_token_stages", "deferred_next",
@@ -99,7 +100,12 @@ def _declare(L: ctypes.CDLL) -> ctypes.CDLL:
     L.flexctc_check.argtypes = [vp, P(ctypes.c_uint32)]
     L.flexctc_host_scratch_bytes.argtypes = [i32, i32, i32, P(Config)]
     L.flexctc_host_scratch_bytes.restype = sz
-    L.flexctc_decode_host.argtypes = [vp, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, vp, vp, vp, vp]
+    L.flexctc_decode_host.argtypes = [vp, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, vp, vp, vp, vp,
+                                      P(ctypes.c_uint32)]
+    L.flexctc_host_scratch_bytes_bf16.argtypes = [i32, i32, i32, P(Config)]
+    L.flexctc_host_scratch_bytes_bf16.restype = sz
+    L.flexctc_decode_host_bf16.argtypes = [vp, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp, vp, vp, vp, vp,
+                                           P(ctypes.c_uint32)]
     L.flexctc_host_streaming.argtypes = []
     L.flexctc_host_streaming.restype = i32
     L.flexctc_set_profile_events.argtypes = [vp, vp]
@@ -187,6 +193,23 @@ class Boost:
         return d.value, nx.value, u.value
 
 
+def _check_lengths(lengths, B: int, device=None, host: bool = False):
+    """lengths must be int32, contiguous, exactly B entries, on log_probs' device (or on the host
+    for decode_host): the C ABI reads int32[B] (an int64 tensor would be misread silently)."""
+    import torch
+    if not isinstance(lengths, torch.Tensor):
+        raise FlexCTCError(1, "lengths must be a torch tensor")
+    if lengths.dtype != torch.int32:
+        raise FlexCTCError(1, f"lengths must be int32 (got {lengths.dtype})")
+    if not lengths.is_contiguous() or lengths.dim() != 1 or lengths.numel() != B:
+        raise FlexCTCError(1, f"lengths must be a contiguous 1-D tensor of B = {B} entries")
+    if host:
+        if lengths.is_cuda:
+            raise FlexCTCError(1, "decode_host takes host lengths")
+    elif not lengths.is_cuda or (device is not None and lengths.device != device):
+        raise FlexCTCError(1, "lengths must be on the same CUDA device as the inputs")
+
+
 def workspace_bytes(B: int, T: int, Vp1: int, cfg: Config) -> int:
     return int(lib.flexctc_workspace_bytes(int(B), int(T), int(Vp1), ctypes.byref(cfg)))
 
@@ -228,9 +251,8 @@ def decode(log_probs, lengths, cfg: Config, lm: LM | None = None, boost: Boost |
         raise FlexCTCError(1, "decode needs CUDA tensors (there is no CPU path)")
     if log_probs.dtype != torch.float32 or log_probs.dim() != 3 or log_probs.stride(2) != 1:
         raise FlexCTCError(1, "log_probs must be float32 [B, T, V'] with unit stride on V'")
-    if lengths.dtype != torch.int32:
-        raise FlexCTCError(1, "lengths must be int32")
     B, T, W = log_probs.shape
+    _check_lengths(lengths, B, log_probs.device)
     Vp1 = W if Vp1 is None else Vp1
     dev = log_probs.device
     if workspace is None:
@@ -266,6 +288,7 @@ def decode_nbest(log_probs, lengths, cfg: Config, nbest: int, lm: LM | None = No
     if log_probs.dtype != torch.float32 or log_probs.dim() != 3 or log_probs.stride(2) != 1:
         raise FlexCTCError(1, "log_probs must be float32 [B, T, V'] with unit stride on V'")
     B, T, W = log_probs.shape
+    _check_lengths(lengths, B, log_probs.device)
     Vp1 = W if Vp1 is None else Vp1
     dev = log_probs.device
     if workspace is None:
@@ -296,6 +319,7 @@ def decode_logits_bf16(logits, lengths, cfg: Config, lm: LM | None = None, boost
     if logits.dtype != torch.bfloat16 or logits.dim() != 3 or logits.stride(2) != 1:
         raise FlexCTCError(1, "logits must be bfloat16 [B, T, V'] with unit stride on V'")
     B, T, W = logits.shape
+    _check_lengths(lengths, B, logits.device)
     Vp1 = W if Vp1 is None else Vp1
     dev = logits.device
     if workspace is None:
@@ -351,27 +375,45 @@ def host_streaming() -> bool:
 def decode_host(log_probs: np.ndarray, lengths: np.ndarray, cfg: Config, lm: LM | None = None,
                 boost: Boost | None = None, scratch=None, stream=None, out=None):
     """End-to-end flexctc_decode_host: host (ideally pinned) float32 [B, T, V'] in, host outputs
-    out; H2D, decode and D2H all run inside the call (which synchronises the stream)."""
+    out; H2D, decode and D2H all run inside the call (which synchronises the stream). The
+    device flags of the decode come back in out["flags"]."""
+    return _decode_host(log_probs, lengths, cfg, lm, boost, scratch, stream, out, bf16=False)
+
+
+def decode_host_bf16(logits, lengths, cfg: Config, lm: LM | None = None, boost: Boost | None = None,
+                     scratch=None, stream=None, out=None):
+    """flexctc_decode_host_bf16: host (ideally pinned) bf16 logits [B, T, V'] (torch.bfloat16, or
+    uint16 bit patterns), normalised on the GPU (reading R25); otherwise as decode_host."""
+    return _decode_host(logits, lengths, cfg, lm, boost, scratch, stream, out, bf16=True)
+
+
+def _decode_host(x, lengths, cfg, lm, boost, scratch, stream, out, bf16):
     import torch
-    if isinstance(log_probs, np.ndarray):
-        log_probs = torch.from_numpy(log_probs)
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(x)
     if isinstance(lengths, np.ndarray):
         lengths = torch.from_numpy(lengths)
-    assert log_probs.dtype == torch.float32 and log_probs.is_contiguous() and not log_probs.is_cuda
-    assert lengths.dtype == torch.int32 and lengths.is_contiguous() and not lengths.is_cuda
-    B, T, Vp1 = log_probs.shape
+    want = (torch.bfloat16, torch.uint16) if bf16 else (torch.float32,)
+    if x.dtype not in want or x.dim() != 3 or not x.is_contiguous() or x.is_cuda:
+        raise FlexCTCError(1, f"decode_host{'_bf16' if bf16 else ''} takes a contiguous host {want[0]} [B, T, V'] tensor")
+    B, T, Vp1 = x.shape
+    _check_lengths(lengths, B, host=True)
+    nscratch = (lib.flexctc_host_scratch_bytes_bf16 if bf16 else lib.flexctc_host_scratch_bytes)(
+        int(B), int(T), int(Vp1), ctypes.byref(cfg))
     if scratch is None:
-        scratch = torch.empty(max(host_scratch_bytes(B, T, Vp1, cfg), 1), dtype=torch.uint8, device="cuda")
+        scratch = torch.empty(max(int(nscratch), 1), dtype=torch.uint8, device="cuda")
     if out is None:
-        pin = log_probs.is_pinned()
+        pin = x.is_pinned()
         out = {"tokens": torch.empty((B, T), dtype=torch.int32, pin_memory=pin),
                "num_tokens": torch.empty(B, dtype=torch.int32, pin_memory=pin),
                "scores": torch.empty(B, dtype=torch.float32, pin_memory=pin),
                "timestamps": torch.empty((B, T), dtype=torch.int32, pin_memory=pin)}
     if stream is None:
         stream = torch.cuda.current_stream()
-    _check(lib.flexctc_decode_host(_ptr(log_probs), _ptr(lengths), B, T, Vp1, ctypes.byref(cfg),
-                                   lm.h if lm else None, boost.h if boost else None, _ptr(scratch),
-                                   scratch.numel(), ctypes.c_void_p(stream.cuda_stream), _ptr(out["tokens"]),
-                                   _ptr(out["num_tokens"]), _ptr(out["scores"]), _ptr(out["timestamps"])))
+    flags = ctypes.c_uint32()
+    fn = lib.flexctc_decode_host_bf16 if bf16 else lib.flexctc_decode_host
+    _check(fn(_ptr(x), _ptr(lengths), B, T, Vp1, ctypes.byref(cfg), lm.h if lm else None, boost.h if boost else None,
+              _ptr(scratch), scratch.numel(), ctypes.c_void_p(stream.cuda_stream), _ptr(out["tokens"]),
+              _ptr(out["num_tokens"]), _ptr(out["scores"]), _ptr(out["timestamps"]), ctypes.byref(flags)))
+    out["flags"] = flags.value
     return out

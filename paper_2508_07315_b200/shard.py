@@ -35,6 +35,17 @@ def gather_results(local: dict, index, B_total: int, T: int, group=None, device=
 
     ws = dist.get_world_size(group)
     dev = device if device is not None else local["tokens"].device
+    # ranks may hold different padded lengths (ragged batches): pad every row to the largest
+    tm = torch.tensor([int(local["tokens"].shape[1])], dtype=torch.int64, device=dev)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX, group=group)
+    T = max(T, int(tm.item()))
+    local = dict(local)
+    for k in ("tokens", "timestamps"):
+        x = local[k]
+        if x.shape[1] < T:
+            y = torch.full((x.shape[0], T), -1, dtype=x.dtype, device=x.device)
+            y[:, : x.shape[1]] = x
+            local[k] = y
     n = torch.tensor([len(index)], dtype=torch.int64, device=dev)
     ns = [torch.zeros_like(n) for _ in range(ws)]
     dist.all_gather(ns, n, group=group)

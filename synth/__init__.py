@@ -346,10 +346,12 @@ def lengths(wl: Workload, B: int | None = None, seed: int | None = None) -> np.n
 
 def logprobs(B: int, T: int, V: int, L: np.ndarray, seed: int, phrase_list: list | None = None,
              token_rate: float = 0.16, pad_value: float = 0.0, row_stride: int | None = None,
-             flat: bool = False, markov_seed: int = LM_SEED):
+             flat: bool = False, markov_seed: int = LM_SEED, return_frames: bool = False):
     """Parakeet-CTC-like log-softmax output, blank = V (last index).
 
-    Returns (D float32 [B, T, stride] with the first V+1 columns valid, transcripts list).
+    Returns (D float32 [B, T, stride] with the first V+1 columns valid, transcripts list), plus,
+    with return_frames, the planted spike frame of every transcript token (the first frame of
+    its span; the RNG stream is the same either way).
     Recipe: logits N(0,1); target (blank on non-spike frames) + U(14,20)
     (U(4,8) for the 'flat' stress variant); on spike frames, p=0.25 a competitor + U(10,16)
     (half random token, half a boosted-phrase continuation); p=0.3 the spike leaks + U(8,14)
@@ -362,6 +364,7 @@ def logprobs(B: int, T: int, V: int, L: np.ndarray, seed: int, phrase_list: list
     src = MarkovSource(V, markov_seed) if V >= 16 else None
     D = np.full((B, T, stride), pad_value, dtype=np.float32)
     transcripts = []
+    spike_frames = []
     tlo, thi = (4.0, 8.0) if flat else (14.0, 20.0)
     for b in range(B):
         Lb = int(L[b])
@@ -385,6 +388,10 @@ def logprobs(B: int, T: int, V: int, L: np.ndarray, seed: int, phrase_list: list
             q = np.sort(rng.integers(0, Lb - 2 * n_tok + 1, n_tok))
             pos = q + 2 * np.arange(n_tok)
             target[pos] = y
+            spike_frames.append([int(x) for x in pos])
+        else:
+            spike_frames.append([])
+        if n_tok > 0:
             for i in range(n_tok):
                 nxt = pos[i + 1] if i + 1 < n_tok else Lb
                 same_next = i + 1 < n_tok and y[i + 1] == y[i]
@@ -405,6 +412,8 @@ def logprobs(B: int, T: int, V: int, L: np.ndarray, seed: int, phrase_list: list
         m = logits.max(axis=1, keepdims=True)
         lse = m + np.log(np.exp(logits - m).sum(axis=1, keepdims=True))
         D[b, :Lb, :Vp1] = (logits - lse).astype(np.float32)
+    if return_frames:
+        return D, transcripts, spike_frames
     return D, transcripts
 
 

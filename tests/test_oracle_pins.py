@@ -316,3 +316,76 @@ def test_log_softmax_bf16_matches_numpy_fp64():
     assert (np.abs(out.astype(np.float64) - ref) <= ulp).all()
     assert (out == ref).mean() > 0.9999
     assert np.allclose(np.exp(out.astype(np.float64)).sum(-1), 1.0, atol=1e-5)
+
+
+# ---------------------------------------------------------------- timestamps and tie rules (round 2)
+
+def _peaky(align, Vp1, p):
+    """log-probs putting p on align[t] and (1-p)/(V'-1) on every other label of frame t"""
+    D = np.full((len(align), Vp1), (1.0 - p) / (Vp1 - 1))
+    D[np.arange(len(align)), align] = p
+    return np.log(D)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_timestamps_hand_fixtures(golden, mode):
+    """R20 timestamps = emission frames of the survivor's alignment (tests/golden 'timestamps')."""
+    g = golden["decode"]["timestamps"]
+    for case in g["cases"]:
+        D = _peaky(case["align"], 3, g["p_target"]).astype(np.float32)[None]
+        out = oracle.decode(D, [len(case["align"])], oracle.make_cfg(4, merge_mode=mode), with_alignment=True)
+        n = int(out["num_tokens"][0])
+        assert out["tokens"][0, :n].tolist() == case["tokens"]
+        assert out["timestamps"][0, :n].tolist() == case["timestamps"]
+        assert out["alignment"][0, :len(case["align"])].tolist() == case["align"]
+        assert (out["timestamps"][0, n:] == -1).all() and (out["tokens"][0, n:] == -1).all()
+
+
+def test_timestamps_match_planted_spikes():
+    """Weak pin of R20 (SURVEY §8(c) 'Unpinned'): on peaky synthetic data the best path emits its
+    tokens at the planted spike frames. 8 c2-shaped utterances (V=1024, no fusion; competitor
+    spikes cause some substitutions and insertions): the fraction of decoded tokens whose
+    timestamp is a planted spike frame of the utterance must be >= 0.95, and the tokens that
+    match the planted one at that frame must be >= 0.85 of all decoded tokens."""
+    import synth
+    wl = synth.WORKLOADS["c2"]
+    L = synth.lengths(wl, 8, wl.seed)
+    D, tr, frames = synth.logprobs(8, wl.T, wl.V, L, wl.seed, return_frames=True)
+    out = oracle.decode(D, L, oracle.make_cfg(wl.beam, beta=wl.beta, theta=wl.theta), nthreads=8)
+    at_spike = same = tot = 0
+    for b in range(8):
+        n = int(out["num_tokens"][b])
+        planted = dict(zip(frames[b], tr[b]))
+        for tok, ts in zip(out["tokens"][b, :n].tolist(), out["timestamps"][b, :n].tolist()):
+            tot += 1
+            at_spike += int(ts in planted)
+            same += int(planted.get(ts) == tok)
+    assert tot > 400
+    assert at_spike / tot >= 0.95, at_spike / tot
+    assert same / tot >= 0.85, same / tot
+
+
+def test_topk_tie_rule(golden):
+    """SPEC S:342 / R9: equal candidates -> the lower flat index enters the TopK (tests/golden 'topk_tie')."""
+    g = golden["decode"]["topk_tie"]
+    D = np.log(np.array(g["D"]))
+    res = oracle.decode_nbest(D, oracle.make_cfg(g["beam"]))
+    assert [list(t) for t, _ in res] == g["nbest_tokens"]
+    assert res[0][1] == res[1][1]
+    D32 = D.astype(np.float32)[None]
+    out = oracle.decode(D32, [1], oracle.make_cfg(g["beam"]))
+    assert out["tokens"][0, :int(out["num_tokens"][0])].tolist() == g["nbest_tokens"][0]
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_merge_tie_rule(golden, mode):
+    """SPEC S:98 / R12, R14: equal-score members of a merge group -> the lower slot survives; its
+    alignment decides the timestamps (tests/golden 'merge_tie')."""
+    g = golden["decode"]["merge_tie"]
+    D = np.log(np.array(g["D"], dtype=np.float64)).astype(np.float32)[None]
+    out = oracle.decode(D, [2], oracle.make_cfg(g["beam"], merge_mode=mode), with_alignment=True)
+    assert out["tokens"][0, :int(out["num_tokens"][0])].tolist() == g["tokens"]
+    assert out["timestamps"][0, :1].tolist() == g["timestamps"]
+    assert out["alignment"][0].tolist() == g["alignment"]
+    want = math.log(0.5) + math.log(0.7) if mode == 1 else math.log(0.85)
+    assert float(out["scores"][0]) == pytest.approx(want, abs=1e-6)

@@ -118,6 +118,9 @@ typedef struct {
     float theta;                  /* θ-prune; +INFINITY disables pruning (R10) */
     int32_t merge_mode;           /* 0 = log-sum-exp (default), 1 = max (R13) */
     int32_t retract_boost_at_eos; /* 1: score -= α_BT·U(state) at EOS (R17); default 0 */
+    int32_t fuse_repeats;         /* 1: repeat candidates (w == last label) also get the α_LM / α_BT
+                                     terms, at every occurrence (the variant the
+                                     authors tried; no β, no state advance); default 0 = Alg. 1 */
 } flexctc_config;
 
 /* Workspace bytes for a decode of B utterances of up to T frames with V+1 = Vp1 tokens.

@@ -316,6 +316,11 @@ std::vector<std::pair<Hyp<R>, int>> decode_utt(const std::vector<std::vector<R>>
                         s = s + beta;                        // P:127 (R8)
                         if (lm) s = fma_r(alpha_lm, (*lr)[w], s);
                         if (bt) s = fma_r(alpha_bt, (*br)[w], s);
+                    } else if (cfg->fuse_repeats && w != blank) {
+                        // P:167 variant: the repeated emission is scored by the LM / BT at each
+                        // occurrence (no β, no state advance: the prefix is unchanged)
+                        if (lm) s = fma_r(alpha_lm, (*lr)[w], s);
+                        if (bt) s = fma_r(alpha_bt, (*br)[w], s);
                     }
                 }
                 cand[f] = Cand<R>{s, f};

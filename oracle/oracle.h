@@ -29,6 +29,7 @@ typedef struct {
     double theta;          /* θ-prune (Alg. 1); +inf disables */
     int32_t merge_mode;    /* 0 = log-sum-exp, 1 = max (R13) */
     int32_t retract_boost_at_eos; /* DESIGN.md R17; default 0 */
+    int32_t fuse_repeats;  /* 1: repeat candidates also get the LM / BT terms (PAPER.md P:167 variant) */
 } oracle_cfg;
 
 const char* oracle_last_error(void);

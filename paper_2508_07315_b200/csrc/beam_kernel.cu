@@ -539,6 +539,21 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     if (al) {
                         sbk = __fadd_rn(a, row[blank]);                 // blank: no β / fusion
                         if (lk != blank) srk = __fadd_rn(a, row[lk]);    // repeat: no β / fusion
+                        if (lk != blank && p.fuse_rep) {
+                            // P:167 variant: the repeated emission is scored by the LM / BT at every
+                            // occurrence (R19 order, no β; the states do not advance)
+                            if (bt_on) {
+                                const int2 e = cur.bts[tid] == 0 ? btroot[lk] : __ldg(&p.bt.tab[(size_t)cur.bts[tid] * V + lk]);
+                                if (lm_on) {
+                                    int nx;
+                                    srk = __fmaf_rn(p.alpha_lm, lm_query<LMV>(p.lm, cur.rec + tid * RWS, lk, nx), srk);
+                                }
+                                srk = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), srk);
+                            } else if (lm_on) {
+                                int nx;
+                                srk = __fmaf_rn(p.alpha_lm, lm_query<LMV>(p.lm, cur.rec + tid * RWS, lk, nx), srk);
+                            }
+                        }
                         float ub = p.beta;
                         if (lm_on) ub += p.alpha_lm * __int_as_float(cur.rec[tid * RWS + 4]);
                         if (bt_on) ub += p.alpha_bt * cur.btm[2 * tid];
@@ -1405,7 +1420,7 @@ int launch_lmv(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, std
 // 1-best output and device-resident input; FLEXCTC_WARP=0 keeps the persistent CTA kernel (test
 // switch: both paths are parity-tested).
 bool use_warp_path(const DecodeParams& p) {
-    if (p.K < 2 || p.K > 32 || p.nbest > 1 || p.ready || !p.cmp || !p.rowoff) return false;
+    if (p.K < 2 || p.K > 32 || p.nbest > 1 || p.ready || !p.cmp || !p.rowoff || p.fuse_rep) return false;
     const char* e = getenv("FLEXCTC_WARP");
     if (e && e[0] == '0') return false;
     if (!(e && e[0] == '1')) {
@@ -1429,7 +1444,7 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
     // K = 1 runs the greedy kernels (greedy_kernel.cu); FLEXCTC_GREEDY=0 keeps the beam kernel
     // (test switch: the two must agree)
     const char* e_gr = getenv("FLEXCTC_GREEDY");
-    const bool greedy = p.K == 1 && p.greedy_sum && !(e_gr && e_gr[0] == '0');
+    const bool greedy = p.K == 1 && p.greedy_sum && !(e_gr && e_gr[0] == '0') && !p.fuse_rep;
     const bool plain = greedy && !p.use_lm && !p.use_bt && p.beta == 0.0f;
     if (!plain) {  // the plain greedy path clamps lengths itself and needs no order
         order_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p.lengths, p.B, p.T, p.order, p.len_c, p.flags, p.B <= 16384);

@@ -109,7 +109,7 @@ struct DecodeParams {
     const int32_t* lengths;
     int32_t B, T, Vp1, K;
     float alpha_lm, alpha_bt, beta, theta;
-    int32_t merge_mode, retract;
+    int32_t merge_mode, retract, fuse_rep;
     int32_t use_lm, use_bt;
     int32_t solo_off;     // tuning/test switch: disable the beam-warp + helpers mode
     // streamed input (flexctc_decode_host): frames [0, *ready) of every utterance have landed in

@@ -221,3 +221,23 @@ def test_sharded_decode_matches_single_rank(lm_pair, bt_pair):
     assert np.array_equal(got["tokens"], ref["tokens"])
     assert np.array_equal(got["timestamps"], ref["timestamps"])
     assert np.array_equal(got["scores"].view(np.int32), ref["scores"].view(np.int32))
+
+
+@pytest.mark.parametrize("wname,B,K,mode", [("c4", 12, 16, 0), ("c4", 12, 16, 1), ("c3", 8, 16, 0), ("c5", 6, 128, 0),
+                                            ("c4", 6, 1, 0), ("c4", 6, 4, 1)])
+def test_fuse_repeats_variant(lm_pair, bt_pair, wname, B, K, mode):
+    """the P:167 variant (LM / BT also on every repeated emission) on the GPU
+    (the CTA kernel: K = 1 and the warp path route there) against the oracle's flag."""
+    wl, D, L, _, _ = synth.workload_inputs(wname, B=B)
+    glm, olm = (lm_pair[0], lm_pair[1]) if wl.lm else (None, None)
+    gbt, obt = (bt_pair[0], bt_pair[1]) if wl.boost else (None, None)
+    run_pair(D, L, wl_cfg(wl, beam=K, merge_mode=mode, fuse_repeats=1), glm, olm, gbt, obt,
+             ctx=f"fuse_repeats {wname} K{K}")
+
+
+def test_fuse_repeats_changes_scores(lm_pair, bt_pair):
+    """The flag is live: on c4 utterances with repeated spikes the scores differ from Alg. 1."""
+    wl, D, L, _, _ = synth.workload_inputs("c4", B=8)
+    a = gpu_decode(D, L, wl_cfg(wl, fuse_repeats=1), lm_pair[0], bt_pair[0])
+    b = gpu_decode(D, L, wl_cfg(wl), lm_pair[0], bt_pair[0])
+    assert (a["scores"] != b["scores"]).any()

@@ -389,3 +389,36 @@ def test_merge_tie_rule(golden, mode):
     assert out["alignment"][0].tolist() == g["alignment"]
     want = math.log(0.5) + math.log(0.7) if mode == 1 else math.log(0.85)
     assert float(out["scores"][0]) == pytest.approx(want, abs=1e-6)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_full_beam_equals_path_enumeration(mode, fuse):
+    """The path-level enumerator (every alignment scored on its own, then combined per transcript)
+    agrees with the full beam, both for Alg. 1 and for the P:167 variant that scores every
+    repeated emission with the LM / BT (fuse_repeats): the variant's extra terms depend only on
+    (prefix, last label), so recombination stays exact."""
+    from tests.exact.exhaustive import exhaustive_paths
+    syms = ["a", "b", "c"]
+    path = os.path.join(GOLDEN, "arpa_3gram.arpa")
+    lm = oracle.LM(path, 3, syms)
+    py = ArpaPy(path)
+    phrases = [[0, 1], [1, 2], [0, 1, 2], [2, 2, 0], [1, 1]]
+    bt = oracle.Boost(phrases, 0.7, 3)
+    bpy = BoostPy(phrases, 0.7)
+    rng = np.random.default_rng(23 + mode + 2 * fuse)
+    Vp1 = 4
+    for T in [1, 2, 3, 4, 5]:
+        D = _rand_logprobs(rng, T, Vp1)
+        cfg = oracle.make_cfg(Vp1 ** T, alpha_lm=0.6, alpha_bt=0.8, beta=0.3, merge_mode=mode, fuse_repeats=fuse)
+        res = dict(oracle.decode_nbest(D, cfg, lm=lm, boost=bt))
+        ex = exhaustive_paths(D, Vp1 - 1, "lse" if mode == 0 else "max", alpha_lm=0.6, lm=py, symbols=syms,
+                              alpha_bt=0.8, boost=bpy, beta=0.3, fuse_repeats=bool(fuse))
+        assert set(res) == set(ex)
+        for y, s in ex.items():
+            assert res[y] == pytest.approx(s, abs=1e-10), (T, y, fuse)
+    if fuse:  # the variant changes scores of transcripts whose alignments repeat a token
+        D = _rand_logprobs(np.random.default_rng(5), 3, Vp1)
+        a = dict(oracle.decode_nbest(D, oracle.make_cfg(64, alpha_lm=0.6, fuse_repeats=1), lm=lm))
+        b = dict(oracle.decode_nbest(D, oracle.make_cfg(64, alpha_lm=0.6, fuse_repeats=0), lm=lm))
+        assert a[()] == b[()] and any(abs(a[y] - b[y]) > 1e-6 for y in a if y)

@@ -329,11 +329,11 @@ def run_flexctc(args):
     stream = torch.cuda.Stream(dev)
     out = None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # per step: decode start/stop, beam kernel start/stop (stage 0), compaction pass start/stop (stage 1)
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(6)) for _ in range(args.steps)]
     for e in ev:  # torch creates events lazily: record once so the C hook gets real cudaEvent_t handles
-        e[2].record(stream)
-        e[3].record(stream)
+        for x in e[2:]:
+            x.record(stream)
 
     def step(e=None):
         nonlocal out
@@ -341,18 +341,22 @@ def run_flexctc(args):
             flush.fill_(1)  # evict L2 (126 MB) between steps; not timed
             if e is not None:
                 e[0].record(stream)
-                FX.set_profile_events(e[2], e[3])
+                FX.set_stage_events(0, e[2], e[3])
+                FX.set_stage_events(1, e[4], e[5])
             if bf16:
                 out = F.decode_logits_bf16(Dd, Ld, cfg, lm, bt, workspace=ws, stream=stream, outputs=out)
             else:
                 out = F.decode(Dd, Ld, cfg, lm, bt, workspace=ws, stream=stream, outputs=out)
             if e is not None:
                 e[1].record(stream)
-                FX.set_profile_events(None, None)
+                FX.set_stage_events(0, None, None)
+                FX.set_stage_events(1, None, None)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    kernel_name = FX.last_kernel()
+    compacted = kernel_name.startswith("warp_beam_kernel")  # the warp path runs the compaction pass
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -370,13 +374,15 @@ def run_flexctc(args):
     torch.cuda.synchronize()
     t_dec = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3        # s, whole decode per step summed
     t_kern = sum(e[2].elapsed_time(e[3]) for e in ev) / 1e3       # s, beam kernel only
+    t_cmp = sum(e[4].elapsed_time(e[5]) for e in ev) / 1e3  # s, compaction pass (0 when it did not run)
+    compacted = compacted or t_cmp > 1e-6
     t_dec_local = t_dec
     flags = F.check(ws)
     dstats = FX.stats(ws)  # device counters of the last timed decode
-    tt = torch.tensor([t_dec, t_kern], dtype=torch.float64, device=dev)
+    tt = torch.tensor([t_dec, t_kern, t_cmp], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    t_dec, t_kern = float(tt[0]), float(tt[1])
+    t_dec, t_kern, t_cmp = float(tt[0]), float(tt[1]), float(tt[2])
     frames_local = float(L.sum())
     frames_all = frames_local * world  # weak scaling: same frame count per rank (c4: fixed T)
     if world > 1:
@@ -402,8 +408,19 @@ def run_flexctc(args):
     #  beam kernel:         Σ_b L_b · (4·V' [read D once] + 3·K [u8 parent + u16 label backpointers])
     #  plain greedy (K=1):  frame_top2_kernel, Σ_b L_b · (4·V' + 16 [{d1, w1, d2} frame summary])
     #  fused greedy (K=1):  greedy_fused_kernel, Σ_b L_b · 4·V'
+    #  warp path (2 <= K <= 32): warp_beam_kernel reads each frame's row (4·V', or 2·V' bf16 logits)
+    #                       and its 256-B record, writes 3·K B of backpointers; the compaction pass
+    #                       reads the row and writes the record: Σ_b L_b · (4·V' + 256) (its own entry)
     plain_greedy = wl.beam == 1 and not wl.lm and not wl.boost and wl.beta == 0.0
-    if wl.beam > 1:
+    xb = 2 if bf16 else 4
+    roof_cmp = None
+    if wl.beam > 1 and compacted:
+        alg_bytes = frames_local * (xb * Vp1 + 256 + 3 * wl.beam)
+        kname = kernel_name + " (beam warp per utterance" + (" + helper warps)" if "helpers" in kernel_name else ")")
+        note = ("latency-bound recurrence: T_max dependent frame steps; the HBM stream of D is the "
+                "compaction pass (roofline_compact); see DESIGN.md")
+        cmp_bytes = frames_local * (xb * Vp1 + 256)
+    elif wl.beam > 1:
         alg_bytes, kname = frames_local * (4 * Vp1 + 3 * wl.beam), "ctc_beam_kernel (persistent)"
         note = "latency-bound recurrence: T_max dependent frame steps; see DESIGN.md"
     elif plain_greedy:
@@ -415,7 +432,17 @@ def run_flexctc(args):
     kern_s = t_kern / args.steps
     achieved = alg_bytes / kern_s / 1e9
     peak, peak_src = peaks()
-    traffic, traffic_src = ncu_traffic(args.workload if not args.beam else f"{args.workload}_k{args.beam}")
+    tkey = (args.workload if not args.beam else f"{args.workload}_k{args.beam}") + ("_bf16" if bf16 else "")
+    traffic, traffic_src = ncu_traffic(tkey)
+    if wl.beam > 1 and compacted and t_cmp > 0:
+        cmp_s = t_cmp / args.steps
+        ctraffic, ctraffic_src = ncu_traffic(tkey + "_compact")
+        roof_cmp = {"bound": "hbm", "achieved": cmp_bytes / cmp_s / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": cmp_bytes / cmp_s / 1e9 / peak, "traffic": ctraffic,
+                    "kernel": "frame_compact_kernel (every valid row once, 8 rows per warp)",
+                    "kernel_ms": 1e3 * cmp_s, "algorithmic_bytes_per_launch": cmp_bytes,
+                    "peak_source": peak_src, "traffic_source": ctraffic_src,
+                    "share_of_step": cmp_s / (t_dec / args.steps)}
 
     # e2e through the public host-buffer entry (flexctc_decode_host): H2D + decode + D2H per step
     e2e = None
@@ -482,14 +509,18 @@ def run_flexctc(args):
                          "traffic_source": traffic_src,
                          "note": note},
             # our kernels per decode: order_kernel (not on the plain greedy path), l2_warm_kernel (with
-            # LM or boost), then the beam kernel, or frame_summary_kernel + greedy_chain/fused kernel
+            # LM or boost), then the beam kernel (warp path: rowoff + compaction + beam kernel), or
+            # frame_summary_kernel + greedy_chain/fused kernel
             "gpu_launches": args.steps * ((0 if plain_greedy else 1) + (1 if (wl.lm or wl.boost) else 0)
-                                          + (1 if wl.beam > 1 else 2)),
+                                          + ((3 if compacted else 1) if wl.beam > 1 else 2)),
             "clocks": clk,
             "e2e": e2e,
+            "kernel": kernel_name,
             "device_flags": flags,
             "device_stats_per_step": dstats,
         }
+        if roof_cmp is not None:
+            res["roofline_compact"] = roof_cmp
         if gathered is not None:
             res["gathered_tokens"] = gathered
         if shards is not None:

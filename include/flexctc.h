@@ -87,6 +87,15 @@ flexctc_status flexctc_lm_get_info(const flexctc_lm* lm, flexctc_lm_info* info);
 flexctc_status flexctc_lm_host_query(const flexctc_lm* lm, int32_t state, int32_t token,
                                      float* logp, int32_t* next_state);
 
+/* Batch form: n (state, token) pairs from host arrays; logp[i], next_state[i] written (host).
+ * FLEXCTC_ERR_INVALID_ARG on a NULL array or any state/token out of range (outputs undefined). */
+flexctc_status flexctc_lm_host_query_batch(const flexctc_lm* lm, int64_t n, const int32_t* states,
+                                           const int32_t* tokens, float* logp, int32_t* next_state);
+
+/* The pre-prune bound the kernels use for a state (test/inspection): *ub >= max over decoder
+ * tokens w of log P(w | state) (nats; rounded up by a relative 1e-5 margin), *eos = LM.Final. */
+flexctc_status flexctc_lm_host_bound(const flexctc_lm* lm, int32_t state, float* ub, float* eos);
+
 /* ---------------------------------------------------------------------------------------
  * GPU-PB replacement (§III-B P:92 "phrase prefix tree ... Aho-Corasick ... boosting
  * scores along the prefix tree based on node depth"; Alg. 1).
@@ -106,6 +115,16 @@ void flexctc_boost_free(flexctc_boost* boost);
 flexctc_status flexctc_boost_host_query(const flexctc_boost* boost, int32_t node, int32_t token,
                                         float* delta, int32_t* next_node, float* U_node);
 flexctc_status flexctc_boost_num_nodes(const flexctc_boost* boost, int32_t* n_nodes);
+
+/* Batch form of flexctc_boost_host_query over n (node, token) pairs (host arrays). */
+flexctc_status flexctc_boost_host_query_batch(const flexctc_boost* boost, int64_t n, const int32_t* nodes,
+                                              const int32_t* tokens, float* delta, int32_t* next_node);
+
+/* Exception signature of a node (test/inspection): bit (token · 0x9E3779B1 mod 2^32) >> 26 is
+ * set for every token whose transition from `node` differs from the root's. For any other token
+ * δ(node, a) = δ(root, a) and delta(node, a) = fl(delta(root, a) - U(node)) exactly, which lets the
+ * kernels serve it from the root row. The root's signature is 0. */
+flexctc_status flexctc_boost_host_signature(const flexctc_boost* boost, int32_t node, uint64_t* sig);
 
 /* ---------------------------------------------------------------------------------------
  * Decoding configuration (Eq. (1) weights P:96-98, θ P:237).
@@ -204,6 +223,19 @@ flexctc_status flexctc_decode_logits_bf16(const uint16_t* logits, int64_t stride
  * persistent beam kernel on the decode stream, so callers can time that kernel alone.
  * Pass NULL, NULL to disable. */
 void flexctc_set_profile_events(void* ev_start, void* ev_stop);
+
+/* Measurement hook per stage of the decode: stage 0 is the beam kernel (the same as
+ * flexctc_set_profile_events), stage 1 the frame compaction pass (the bandwidth-bound pass over
+ * every valid frame row; only decodes that take the warp path, 2 <= K <= 32,
+ * launch it). Events are cudaEvent_t, recorded on the decode stream immediately before and after
+ * the stage's kernel; NULL, NULL disables the stage. Returns FLEXCTC_ERR_INVALID_ARG for an
+ * unknown stage. */
+flexctc_status flexctc_set_stage_events(int32_t stage, void* ev_start, void* ev_stop);
+
+/* Name of the main (frame-loop) kernel the last decode on this thread launched, e.g.
+ * "warp_beam_kernel+helpers", "warp_beam_kernel", "ctc_beam_kernel", "greedy_fused_kernel",
+ * "greedy_chain_kernel" (static string, never NULL; "" before the first decode). */
+const char* flexctc_last_kernel(void);
 
 /* Device counters of the last decode that used `workspace` (call after the stream has
  * synchronised); copies min(n, 32) u64 values: frames, sum of live slots, sum of listed tokens,

@@ -66,6 +66,8 @@ def lib():
         L.oracle_lm_order.argtypes = [vp]
         L.oracle_lm_logp.restype = dbl
         L.oracle_lm_logp.argtypes = [vp, vp, i32, i32, i32]
+        L.oracle_lm_logp_many.restype = None
+        L.oracle_lm_logp_many.argtypes = [vp, vp, i32, vp, i32, i32, vp]
         L.oracle_lm_seq.restype = dbl
         L.oracle_lm_seq.argtypes = [vp, vp, i32]
         L.oracle_boost_build.restype = vp
@@ -121,6 +123,14 @@ class LM:
     @property
     def order(self) -> int:
         return lib().oracle_lm_order(self.h)
+
+    def logp_many(self, hist, ws, f32: bool = False):
+        """log P(w | hist) for every w in ws (float64 array; f32: the fp32 evaluation)."""
+        h = np.ascontiguousarray(hist, dtype=np.int32)
+        w = np.ascontiguousarray(ws, dtype=np.int32)
+        out = np.empty(w.shape[0], dtype=np.float64)
+        lib().oracle_lm_logp_many(self.h, _ptr(h), len(h), w.ctypes.data, w.shape[0], int(f32), out.ctypes.data)
+        return out
 
     def logp(self, hist, w: int, f32: bool = False) -> float:
         """log P(w | <s> hist) in nats; w = -1 means </s>."""

@@ -436,6 +436,18 @@ double oracle_lm_logp(const void* lmv, const int32_t* hist, int32_t n, int32_t w
     return f32 ? (double)lm_logp_sym<float>(a, h, ws) : lm_logp_sym<double>(a, h, ws);
 }
 
+// log P(w | hist) for many tokens after one history (the same evaluator as oracle_lm_logp)
+void oracle_lm_logp_many(const void* lmv, const int32_t* hist, int32_t n, const int32_t* ws, int32_t m, int32_t f32,
+                         double* out) {
+    const Arpa& a = *(const Arpa*)lmv;
+    std::vector<int> prefix(hist, hist + n);
+    std::vector<int> h = lm_history(a, prefix);
+    for (int32_t i = 0; i < m; ++i) {
+        int wsym = ws[i] < 0 ? a.eos : a.tok2sym[ws[i]];
+        out[i] = f32 ? (double)lm_logp_sym<float>(a, h, wsym) : lm_logp_sym<double>(a, h, wsym);
+    }
+}
+
 double oracle_lm_seq(const void* lmv, const int32_t* toks, int32_t n) {
     const Arpa& a = *(const Arpa*)lmv;
     double s = 0;

@@ -40,6 +40,9 @@ void  oracle_lm_free(void* lm);
 int32_t oracle_lm_order(const void* lm);
 /* log P(w | <s> hist[0..n)) in nats; w = decoder token, or -1 for </s>. f32 != 0 -> fp32 path. */
 double oracle_lm_logp(const void* lm, const int32_t* hist, int32_t n, int32_t w, int32_t f32);
+/* the same for m tokens after one history: out[i] = log P(ws[i] | hist) */
+void oracle_lm_logp_many(const void* lm, const int32_t* hist, int32_t n, const int32_t* ws, int32_t m, int32_t f32,
+                         double* out);
 /* Σ_i log P(tok_i | <s> tok_<i) + log P(</s> | <s> tok), fp64 */
 double oracle_lm_seq(const void* lm, const int32_t* toks, int32_t n);
 

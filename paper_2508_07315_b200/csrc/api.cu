@@ -17,7 +17,11 @@ namespace flexctc {
 thread_local std::string g_error;
 thread_local void* g_ev_start = nullptr;
 thread_local void* g_ev_stop = nullptr;
+thread_local void* g_ev_cmp_start = nullptr;  // stage 1: the frame compaction pass
+thread_local void* g_ev_cmp_stop = nullptr;
+thread_local const char* g_kernel = "";
 void set_error(const std::string& msg) { g_error = msg; }
+void set_kernel_name(const char* name) { g_kernel = name; }
 flexctc_status fail(flexctc_status st, const std::string& msg) {
     g_error = msg;
     return st;
@@ -91,7 +95,7 @@ WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K) {
     w.bp_label = o; o += align256((size_t)B * T * K * 2);
     w.align_ws = o; o += align256((size_t)B * T * 4);
     w.greedy = o; o += K == 1 ? align256((size_t)B * T * 16) : 0;  // plain greedy frame summaries
-    const bool warp = K >= 2 && K <= 32;  // the warp-per-utterance path: frame records + row prefix
+    const bool warp = K >= 2;  // frame records + row prefix (compaction pass; every beam path K >= 2)
     w.cmp = o; o += warp ? align256((size_t)B * T * kCmpBytes) : 0;
     w.rowoff = o; o += warp ? align256(8 * ((size_t)B + 1)) : 0;
     w.total = o;
@@ -105,7 +109,8 @@ using namespace flexctc;
 extern "C" {
 
 const char* flexctc_last_error(void) { return g_error.c_str(); }
-const char* flexctc_version(void) { return "flexctc-b200 0.1 (sm_100a)"; }
+const char* flexctc_version(void) { return "flexctc-b200 0.2 (sm_100a)"; }
+const char* flexctc_last_kernel(void) { return g_kernel; }
 
 flexctc_status flexctc_lm_load(const char* arpa_path, int32_t vocab_size, const char* const* token_symbols,
                                int32_t device, flexctc_lm** out) {
@@ -189,6 +194,25 @@ flexctc_status flexctc_lm_host_query(const flexctc_lm* lm, int32_t state, int32_
     return FLEXCTC_OK;
 }
 
+flexctc_status flexctc_lm_host_query_batch(const flexctc_lm* lm, int64_t n, const int32_t* states,
+                                           const int32_t* tokens, float* logp, int32_t* next_state) {
+    if (!lm || n < 0 || (n > 0 && (!states || !tokens || !logp || !next_state)))
+        return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    for (int64_t i = 0; i < n; ++i) {
+        const flexctc_status st = flexctc_lm_host_query(lm, states[i], tokens[i], &logp[i], &next_state[i]);
+        if (st != FLEXCTC_OK) return st;
+    }
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_lm_host_bound(const flexctc_lm* lm, int32_t state, float* ub, float* eos) {
+    if (!lm || !ub || !eos) return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    if (state < 0 || state >= lm->host.S) return fail(FLEXCTC_ERR_INVALID_ARG, "state out of range");
+    *ub = lm->host.ub[state];
+    *eos = lm->host.eos[state];
+    return FLEXCTC_OK;
+}
+
 flexctc_status flexctc_boost_build(const int32_t* tokens, const int64_t* offsets, int32_t n_phrases,
                                    float token_weight, int32_t vocab_size, int32_t device, flexctc_boost** out) {
     if (!out) return fail(FLEXCTC_ERR_INVALID_ARG, "out is NULL");
@@ -203,6 +227,7 @@ flexctc_status flexctc_boost_build(const int32_t* tokens, const int64_t* offsets
         size_t o_tab = up.add(h.tab.data(), h.tab.size() * 4);
         size_t o_u = up.add(h.U.data(), h.U.size() * 4);
         size_t o_m = up.add(h.maxd.data(), h.maxd.size() * 4);
+        size_t o_s = up.add(h.sig.data(), h.sig.size() * 8);
         st = upload(device, up, &bt->dmem);
         if (st != FLEXCTC_OK) { delete bt; return st; }
         bt->dbytes = up.total();
@@ -211,6 +236,7 @@ flexctc_status flexctc_boost_build(const int32_t* tokens, const int64_t* offsets
         bt->dev.tab_bytes = (int64_t)h.tab.size() * 4;
         bt->dev.U = (const float*)(d + o_u);
         bt->dev.maxd = (const float*)(d + o_m);
+        bt->dev.sig = (const unsigned long long*)(d + o_s);
         bt->dev.V = h.V;
     }
     *out = bt;
@@ -238,6 +264,25 @@ flexctc_status flexctc_boost_host_query(const flexctc_boost* bt, int32_t node, i
     *next_node = h.tab[e];
     memcpy(delta, &h.tab[e + 1], 4);
     *U_node = h.U[node];
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_boost_host_query_batch(const flexctc_boost* bt, int64_t n, const int32_t* nodes,
+                                              const int32_t* tokens, float* delta, int32_t* next_node) {
+    if (!bt || n < 0 || (n > 0 && (!nodes || !tokens || !delta || !next_node)))
+        return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    float U = 0.0f;
+    for (int64_t i = 0; i < n; ++i) {
+        const flexctc_status st = flexctc_boost_host_query(bt, nodes[i], tokens[i], &delta[i], &next_node[i], &U);
+        if (st != FLEXCTC_OK) return st;
+    }
+    return FLEXCTC_OK;
+}
+
+flexctc_status flexctc_boost_host_signature(const flexctc_boost* bt, int32_t node, uint64_t* sig) {
+    if (!bt || !sig) return fail(FLEXCTC_ERR_INVALID_ARG, "NULL argument");
+    if (node < 0 || node >= bt->host.N) return fail(FLEXCTC_ERR_INVALID_ARG, "node out of range");
+    *sig = bt->host.sig[node];
     return FLEXCTC_OK;
 }
 
@@ -334,7 +379,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.bp_label = (uint16_t*)(w + wl.bp_label);
     p.align_ws = (int32_t*)(w + wl.align_ws);
     p.greedy_sum = cfg->beam == 1 ? (float4*)(w + wl.greedy) : nullptr;
-    const bool warp_ws = cfg->beam >= 2 && cfg->beam <= 32;
+    const bool warp_ws = cfg->beam >= 2;
     p.cmp = warp_ws ? (uint8_t*)(w + wl.cmp) : nullptr;
     p.rowoff = warp_ws ? (int64_t*)(w + wl.rowoff) : nullptr;
     p.nch = wl.nch;
@@ -358,7 +403,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
         p.stride_b = (int64_t)T * Vp1;
         p.stride_t = Vp1;
     }
-    int rc = launch_decode(p, (void*)stream, g_ev_start, g_ev_stop, err);
+    int rc = launch_decode(p, (void*)stream, g_ev_start, g_ev_stop, err, g_ev_cmp_start, g_ev_cmp_stop);
     if (rc == 2) return fail(FLEXCTC_ERR_CAPACITY, err);
     if (rc != 0) return fail(FLEXCTC_ERR_CUDA, err);
     return FLEXCTC_OK;
@@ -398,6 +443,19 @@ flexctc_status flexctc_decode_logits_bf16(const uint16_t* logits, int64_t stride
 void flexctc_set_profile_events(void* ev_start, void* ev_stop) {
     g_ev_start = ev_start;
     g_ev_stop = ev_stop;
+}
+
+flexctc_status flexctc_set_stage_events(int32_t stage, void* ev_start, void* ev_stop) {
+    if (stage == 0) {
+        g_ev_start = ev_start;
+        g_ev_stop = ev_stop;
+    } else if (stage == 1) {
+        g_ev_cmp_start = ev_start;
+        g_ev_cmp_stop = ev_stop;
+    } else {
+        return fail(FLEXCTC_ERR_INVALID_ARG, "unknown stage");
+    }
+    return FLEXCTC_OK;
 }
 
 flexctc_status flexctc_get_stats(const void* workspace, uint64_t* out, int32_t n) {
@@ -575,8 +633,6 @@ flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* le
         const size_t row = (size_t)Vp1 * esz;
         int Lmin = T;
         for (int b = 0; b < B; ++b) Lmin = std::min(Lmin, std::min(std::max(lengths_host[b], 0), T));
-        std::vector<void*> dsts, srcs;
-        std::vector<size_t> sizes;
         const char* xh = (const char*)x_host;
         int t0 = 0;
         for (int t1 : chunk_ends(T)) {
@@ -584,29 +640,19 @@ flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* le
                 e = cudaMemcpy2DAsync(dIn + (size_t)t0 * row, (size_t)T * row, xh + (size_t)t0 * row,
                                       (size_t)T * row, row * (size_t)(t1 - t0), (size_t)B, cudaMemcpyHostToDevice,
                                       g_host.copy);
-            } else {  // ragged: one batched copy of the valid frames of each utterance
-                dsts.clear(); srcs.clear(); sizes.clear();
-                for (int b = 0; b < B; ++b) {
-                    const int L = std::min(std::max(lengths_host[b], 0), T);
-                    if (L <= t0) continue;
+            } else {
+                // ragged: one 2D copy of the whole chunk per maximal run of consecutive utterances
+                // with L_b > t0 (an utterance ending inside the chunk also gets its padding rows
+                // [L_b, t1) of the caller's buffer: never read by the decode)
+                for (int b = 0; b < B && e == cudaSuccess;) {
+                    auto alive = [&](int i) { return std::min(std::max(lengths_host[i], 0), T) > t0; };
+                    if (!alive(b)) { ++b; continue; }
+                    int b1 = b + 1;
+                    while (b1 < B && alive(b1)) ++b1;
                     const size_t off = ((size_t)b * T + t0) * row;
-                    dsts.push_back(dIn + off);
-                    srcs.push_back((void*)(xh + off));
-                    sizes.push_back(row * (size_t)(std::min(L, t1) - t0));
-                }
-                if (!dsts.empty()) {
-                    cudaMemcpyAttributes at{};
-                    at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-                    at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-                    size_t ai = 0, fi = 0;
-                    e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &at, &ai, 1, &fi,
-                                             g_host.copy);
-                    if (e != cudaSuccess) {  // runtime without batched copies: one copy per utterance
-                        cudaGetLastError();
-                        e = cudaSuccess;
-                        for (size_t i = 0; i < dsts.size() && e == cudaSuccess; ++i)
-                            e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, g_host.copy);
-                    }
+                    e = cudaMemcpy2DAsync(dIn + off, (size_t)T * row, xh + off, (size_t)T * row,
+                                          row * (size_t)(t1 - t0), (size_t)(b1 - b), cudaMemcpyHostToDevice, g_host.copy);
+                    b = b1;
                 }
             }
             if (e == cudaSuccess && bf16 &&

@@ -73,6 +73,7 @@ struct Bank {
 
 struct Shared {
     float* ring;
+    unsigned char* rring;  // [R][kCmpBytes] frame records (use_cmp)
     Bank bk;  // bank 0; bank 1 of every field starts `K` (or K*stride) elements later
     uint64_t* ckey; int* clm; int* cbt;   // candidate buffer [cap]
     uint64_t* skey; int* slm; int* sbt;   // selection [K]
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         unsigned char* q = smem_raw;
         auto take = [&](size_t bytes) { unsigned char* r = q; q += (bytes + 15) & ~size_t(15); return r; };
         sm.ring = (float*)take(sizeof(float) * (size_t)R * (VP + 4));
+        sm.rring = (unsigned char*)take(p.use_cmp ? (size_t)R * kCmpBytes : 0);
         {
             Bank& B = sm.bk;  // both banks of each field, contiguous
             B.acc = (float*)take(8 * K); B.last = (int*)take(8 * K); B.hash = (uint64_t*)take(16 * K);
@@ -461,6 +463,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 if (r < L) {
                     wait_ready(p, r, ready);
                     load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                    if (p.use_cmp && ltid < kCmpBytes / 16)
+                        cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
+                                   p.cmp + ((int64_t)b * p.T + r) * kCmpBytes + 16 * ltid);
                 }
                 cp_commit();
             }
@@ -478,16 +483,34 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 if (r < L) {
                     wait_ready(p, r, ready);
                     load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                    if (p.use_cmp && ltid < kCmpBytes / 16)
+                        cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
+                                   p.cmp + ((int64_t)b * p.T + r) * kCmpBytes + 16 * ltid);
                 }
                 cp_commit();
                 if (solo) cp_wait<2>(); else if (R == 4) cp_wait<3>(); else cp_wait<1>();
             }
+            // the compaction pass's record of frame t (use_cmp): D[blank], the listed tokens sorted by
+            // (D desc, token asc) and floor >= every unlisted D; n = 0 with floor = +inf: no usable list
+            const unsigned char* rc_t = sm.rring + (size_t)slot * kCmpBytes;
             if (helper) {
                 // frame summary for the beam warp: best non-blank token and the complete list of
                 // tokens within kListDelta of it (capped at 32; the count says when it overflowed)
+                // or, with records, the record's list (band <= 16 nats, <= 32 tokens) and floor
                 const int h = ltid;
-                if (h == 0) s_sum_cnt[slot] = 0;
-                helpers_sync(lnt);  // every helper's cp.async of row t has landed (each waited its own)
+                helpers_sync(lnt);  // every helper's cp.async of row t (and record) has landed
+                const int rn = p.use_cmp ? ((const int*)rc_t)[2] : 0;
+                const float rfl = p.use_cmp ? ((const float*)rc_t)[1] : INFINITY;
+                if (p.use_cmp && !(rn == 0 && rfl == INFINITY)) {
+                    const float* rv = (const float*)(rc_t + 32);
+                    const uint16_t* rt = (const uint16_t*)(rc_t + 160);
+                    if (h < rn) { s_list_tok[slot * kListCap + h] = rt[h]; s_list_d[slot * kListCap + h] = rv[h]; }
+                    if (h == 0) {
+                        s_sum_cnt[slot] = rn;
+                        s_sum_floor[slot] = rfl;
+                        s_sum_key[slot] = rn > 0 ? make_key(rv[0], (uint32_t)rt[0]) : make_key(kNeg, 0u);
+                    }
+                } else {
                 float bv = kNeg;
                 int bi = -1;
                 for (int w = h; w < blank; w += lnt) {
@@ -498,6 +521,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
 #pragma unroll
                 for (int o = 16; o; o >>= 1) key = umax64(key, __shfl_xor_sync(0xffffffffu, key, o));
                 if ((tid & 31) == 0) s_hkey[(tid >> 5) - 1] = key;
+                if (h == 0) s_sum_cnt[slot] = 0;  // ordered before the list atomics by the barrier
                 helpers_sync(lnt);
                 uint64_t best = s_hkey[0];
                 for (int i = 1; i < (lnt >> 5); ++i) best = umax64(best, s_hkey[i]);
@@ -516,6 +540,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     }
                 }
                 if (h == 0) { s_sum_key[slot] = best; s_sum_floor[slot] = floor_; }
+                }  // no usable record
             }
             if (tid == 0) { sc.nbuf = 0; sc.m = 0; sc.npair = 0; }
             __syncthreads();  // B0: row t and its summary are ready
@@ -563,6 +588,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 uint64_t best_tok = 0;
                 if (solo) {
                     best_tok = s_sum_key[slot];
+                } else if (p.use_cmp && !(((const int*)rc_t)[2] == 0 && ((const float*)rc_t)[1] == INFINITY)) {
+                    // the record's best listed token (every unlisted one is <= floor <= it)
+                    const int rn = ((const int*)rc_t)[2];
+                    best_tok = rn > 0 ? make_key(((const float*)(rc_t + 32))[0], (uint32_t)((const uint16_t*)(rc_t + 160))[0])
+                                      : make_key(kNeg, 0u);
                 } else {
                     float bv = kNeg;
                     int bi = -1;
@@ -659,7 +689,20 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const bool scan_all = sc.scan;
             const int nalive = sc.nalive;
             const float ubvmax = sc.ubvmax;
-            if (scan_all) {  // full filter scan of the row by the whole CTA
+            if (scan_all && p.use_cmp && sc.dthr >= ((const float*)rc_t)[1]) {
+                // the record lists every token with D >= floor <= dthr: filter its list
+                const float dthr = sc.dthr;
+                const int excl = sc.excl;
+                const int rn = ((const int*)rc_t)[2];
+                if (tid < 32) {
+                    const int w = tid < rn ? (int)((const uint16_t*)(rc_t + 160))[tid] : -1;
+                    const bool hit = w >= 0 && w != excl && ((const float*)(rc_t + 32))[tid] >= dthr;
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (hit) sm.toks[__popc(bal & ((1u << tid) - 1u))] = (uint16_t)w;
+                    if (tid == 0) sc.m = __popc(bal);
+                }
+                __syncthreads();
+            } else if (scan_all) {  // full filter scan of the row by the whole CTA
                 const float dthr = sc.dthr;
                 const int excl = sc.excl;
                 for (int w0 = 0; w0 < Vp1; w0 += NT) {
@@ -1228,7 +1271,7 @@ __global__ void order_kernel(const int32_t* __restrict__ lengths, int B, int T, 
 size_t smem_bytes(int K, int Vp1, int R, int cap, int nch, int RWS) {
     const int VP = (Vp1 + 3) & ~3;
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-    size_t s = al(sizeof(float) * (size_t)R * (VP + 4));
+    size_t s = al(sizeof(float) * (size_t)R * (VP + 4)) + (size_t)R * kCmpBytes;
     s += al(8 * K) + al(8 * K) + al(16 * K) + al(8 * K) + al(8 * K) + al(2 * K) + al(8 * (size_t)K * RWS) + al(16 * K);
     s += al(8 * (size_t)cap) + 2 * al(4 * (size_t)cap);
     s += al(8 * K) + 2 * al(4 * K);
@@ -1350,6 +1393,7 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
+    set_kernel_name("ctc_beam_kernel");
     return 0;
 }
 
@@ -1425,18 +1469,19 @@ bool use_warp_path(const DecodeParams& p) {
     if (e && e[0] == '0') return false;
     if (!(e && e[0] == '1')) {
         // Up to 4 x #SMs utterances the persistent CTA kernel (2-8 warps per utterance, up to 592
-        // in flight) has the shorter frame step; beyond, the warp kernel's one warp per utterance
-        // packs more utterances per SM (tools/policy_sweep.py, profiles/r2_policy.jsonl)
+        // in flight) has the shorter frame step (the warp kernel's helper mode, opt-in, measured
+        // slower at c4); beyond, the warp kernel's one warp per utterance packs more utterances
+        // per SM (tools/policy_sweep.py, profiles/r2/policy_*.jsonl)
         int dev = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (p.B <= 4 * nsm) return false;
+        if (p.B <= 4 * nsm && !warp_helper_mode(p, nsm)) return false;
     }
     const size_t per = warp_beam_smem_per_warp(p.Vp1, p.logits != nullptr, p.nch);
     return per + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0) <= 200 * 1024;
 }
 
-int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std::string& err) {
+int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std::string& err, void* ev2, void* ev3) {
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(p.flags, 0, 64 + 8 * kStatsWords, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
@@ -1470,13 +1515,29 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
         // K <= 32: the bandwidth-bound compaction pass over every valid row, then one warp per
         // utterance (warp_beam_kernel.cu)
         int rc = launch_rowoff(p.len_c, p.B, p.rowoff, stream, err);
+        if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev2, st);
         if (!rc) rc = launch_compact(p.logits ? (const void*)p.logits : (const void*)p.log_probs, p.logits != nullptr,
                                      p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err);
+        if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev3, st);
         if (!rc) rc = launch_warp_beam(p, p.logits != nullptr, stream, ev0, ev1, err);
         return rc;
     }
     const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
-    return small_lm ? launch_lmv<2>(p, st, ev0, ev1, err) : launch_lmv<kMaxLmLevels>(p, st, ev0, ev1, err);
+    // FLEXCTC_CMP=1: the persistent CTA kernel reads the frame records of the compaction pass (the
+    // best token, the listed band and its floor) instead of computing per-frame summaries from the
+    // rows. Opt-in: the pass costs more than it saves at c4 / c5 (profiles/r2/cta_records_ab.jsonl:
+    // c4 1.661 -> 1.672 ms, c5 5.873 -> 5.961 ms per decode)
+    DecodeParams q = p;
+    const char* e_cmp = getenv("FLEXCTC_CMP");
+    q.use_cmp = p.cmp && p.rowoff && !p.ready && !p.logits && e_cmp && e_cmp[0] == '1' ? 1 : 0;
+    if (q.use_cmp) {
+        int rc = launch_rowoff(p.len_c, p.B, p.rowoff, stream, err);
+        if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev2, st);
+        if (!rc) rc = launch_compact(p.log_probs, false, p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err);
+        if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev3, st);
+        if (rc) return rc;
+    }
+    return small_lm ? launch_lmv<2>(q, st, ev0, ev1, err) : launch_lmv<kMaxLmLevels>(q, st, ev0, ev1, err);
 }
 
 }  // namespace flexctc

@@ -99,6 +99,14 @@ flexctc_status build_boost_host(const int32_t* toks, const int64_t* offs, int32_
         }
         out.maxd[u] = m;
     }
+    // exception signature: bit lm_sig_bit(a) set for every token a whose transition from u differs
+    // from the root's. For any other token, δ(u, a) = δ(root, a) and
+    // delta(u, a) = fl(gain(δ(root, a)) - U(u)) = fl(delta(root, a) - U(u)) exactly (delta(root, a) =
+    // gain(δ(root, a)) since U(root) = 0), so the device needs only the root row and U(u).
+    out.sig.assign(N, 0ull);
+    for (int32_t u = 1; u < N; ++u)
+        for (int32_t a = 0; a < V; ++a)
+            if (nxt[(size_t)u * V + a] != nxt[a]) out.sig[u] |= 1ull << lm_sig_bit(a);
     return FLEXCTC_OK;
 }
 

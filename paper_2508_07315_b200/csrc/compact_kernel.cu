@@ -15,8 +15,8 @@
 // way. The logits are read once at 2 B per element.
 //
 // Rows are addressed through the prefix of the clamped lengths (rowoff, written by
-// order_kernel): the grid covers Σ_b L_b rows, not B·T (LibriSpeech-shaped batches are ~80 %
-// padding at T_max), 8 consecutive rows per warp.
+// rowoff_kernel): the grid covers Σ_b L_b rows, not B·T (LibriSpeech-shaped batches are ~80 %
+// padding at T_max), 4 consecutive rows per warp, each loaded as 16-B blocks into registers.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -32,40 +32,105 @@ namespace {
 using namespace dev;
 
 constexpr int kWarps = 8;        // warps per CTA
-constexpr int kRowsPerWarp = 8;  // consecutive flattened rows per warp
-constexpr int kPerLane = 33;     // register-resident elements per lane (V' <= 1056)
+constexpr int kRowsPerWarp = 4;  // consecutive flattened rows per warp (one utterance lookup each)
+// 16-B blocks per lane held in registers: rows of <= 32·kBlk blocks (V' <= 1149 for fp32 log-probs,
+// <= 1273 for bf16 logits) stay in registers
+template <bool BF16> constexpr int kBlk = BF16 ? 5 : 9;
 
 template <bool BF16>
-__device__ __forceinline__ float ld_x(const void* row, int w) {
-    if constexpr (BF16) return bf16f(__ldg((const uint16_t*)row + w));
-    else return __ldg((const float*)row + w);
+__device__ __forceinline__ float elem(const uint4& q, int j) {  // element j of a 16-B block
+    if constexpr (BF16) {
+        const uint32_t u = j < 2 ? (j == 0 ? q.x : q.x >> 16) : j < 4 ? (j == 2 ? q.y : q.y >> 16)
+                         : j < 6 ? (j == 4 ? q.z : q.z >> 16) : (j == 6 ? q.w : q.w >> 16);
+        return bf16f((uint16_t)(u & 0xffffu));
+    } else {
+        return __uint_as_float(j == 0 ? q.x : j == 1 ? q.y : j == 2 ? q.z : q.w);
+    }
 }
 
-// One row -> one record. `v` holds the row when V' <= 32·kPerLane (the usual shape: one HBM
-// read); larger rows are re-read from L1/L2 by each pass.
+// One row -> one record. The warp loads the row's covering 16-B blocks (LDG.128, evict-first: D
+// is read once) into registers, kBlk per lane; a block lying partly outside [lo, hi) (at most
+// the tensor's first and last row) is assembled element by element from inside the range.
+// Rows longer than 32·kBlk blocks take the generic path (values re-read from L1/L2).
 template <bool BF16>
-__device__ void compact_row(const void* row, int Vp1, uint8_t* rec, uint64_t* keys, int lane) {
+__device__ void compact_row(const void* row, int Vp1, uint8_t* rec, uint64_t* keys, int lane, const char* lo,
+                            const char* hi) {
+    constexpr int EPB = BF16 ? 8 : 4;  // elements per 16-B block
+    constexpr int ESZ = BF16 ? 2 : 4;
     const int blank = Vp1 - 1;
-    const bool in_regs = Vp1 <= 32 * kPerLane;
-    float v[kPerLane];
-    float mn = kNeg;  // max over non-blank
-    float xb = kNeg;  // blank value (logit or D)
+    const char* src = (const char*)row;
+    const char* g = (const char*)((uintptr_t)src & ~(uintptr_t)15);
+    const int off = (int)(src - g) / ESZ;  // element offset of w = 0 inside block 0
+    const int nblk = (off + Vp1 + EPB - 1) / EPB;
+    const bool in_regs = nblk <= 32 * kBlk<BF16>;
+    uint4 q[kBlk<BF16>];
     if (in_regs) {
+        const uint64_t pol = policy_evict_first();
+        const bool all_in = g >= lo && g + 16 * (size_t)nblk <= hi;  // every covering block inside the tensor
 #pragma unroll
-        for (int i = 0; i < kPerLane; ++i) {
-            const int w = lane + 32 * i;
-            v[i] = w < Vp1 ? ld_x<BF16>(row, w) : kNeg;
+        const uint32_t ninf = BF16 ? 0xff80ff80u : 0xff800000u;  // -inf in every element
+        for (int i = 0; i < kBlk<BF16>; ++i) {
+            const int bi = lane + 32 * i;
+            q[i] = make_uint4(ninf, ninf, ninf, ninf);
+            if (bi < nblk) {
+                const char* a = g + 16 * (size_t)bi;
+                if (all_in || (a >= lo && a + 16 <= hi)) {
+                    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                                 : "=r"(q[i].x), "=r"(q[i].y), "=r"(q[i].z), "=r"(q[i].w) : "l"(a), "l"(pol));
+                } else {  // edge block: only the row's own elements
+                    uint16_t h[8] = {};
+                    float f[4] = {};
+                    for (int j = 0; j < EPB; ++j) {
+                        const int w = bi * EPB + j - off;
+                        if (w >= 0 && w < Vp1) {
+                            if constexpr (BF16) h[j] = __ldg((const uint16_t*)src + w);
+                            else f[j] = __ldg((const float*)src + w);
+                        }
+                    }
+                    if constexpr (BF16)
+                        q[i] = make_uint4(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16),
+                                          h[4] | ((uint32_t)h[5] << 16), h[6] | ((uint32_t)h[7] << 16));
+                    else
+                        q[i] = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                                          __float_as_uint(f[3]));
+                }
+            }
         }
-        xb = ld_x<BF16>(row, blank);  // broadcast (L1 hit)
+    }
+    // token index of element slot (i, j) of this lane; v[] = the non-blank values, -inf elsewhere
+    auto tok_of = [&](int i, int j) { return (lane + 32 * i) * EPB + j - off; };
+    auto ld_w = [&](int w) -> float {  // generic path
+        if constexpr (BF16) return bf16f(__ldg((const uint16_t*)src + w));
+        else return __ldg((const float*)src + w);
+    };
+    constexpr int NV = kBlk<BF16> * EPB;
+    float v[NV];
+    float mn = kNeg;  // max over non-blank tokens (NaN never wins)
+    if (in_regs) {
+        // only the row's first block (elements before w = 0) and the blank's block (the blank and
+        // the bytes after it) hold elements that are not non-blank tokens; blocks past the row
+        // were filled with -inf
+        const int bl = (off + blank) / EPB, jb = off + blank - bl * EPB;  // the blank: block, element
 #pragma unroll
-        for (int i = 0; i < kPerLane; ++i)
-            if (lane + 32 * i < blank) mn = fmaxf(mn, v[i]);
+        for (int i = 0; i < kBlk<BF16>; ++i) {
+            const int bi = lane + 32 * i;
+#pragma unroll
+            for (int j = 0; j < EPB; ++j) {
+                const float x = elem<BF16>(q[i], j);
+                const bool out = (i == 0 && bi == 0 && j < off) || (bi == bl && j >= jb);
+                v[i * EPB + j] = out ? kNeg : x;
+            }
+        }
+        float m4[4] = {kNeg, kNeg, kNeg, kNeg};  // independent partial maxima
+#pragma unroll
+        for (int e = 0; e < NV; ++e) m4[e & 3] = fmaxf(m4[e & 3], v[e]);
+        mn = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     } else {
-        xb = ld_x<BF16>(row, blank);
-        for (int w = lane; w < blank; w += 32) mn = fmaxf(mn, ld_x<BF16>(row, w));
+        for (int w = lane; w < blank; w += 32) mn = fmaxf(mn, ld_w(w));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mn = fmaxf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    const float xb = ld_w(blank);  // blank value (logit or D): an L1 hit
 
     double lse = 0.0;
     if constexpr (BF16) {  // R25: m over every logit, S in fp64, lse = m + log S
@@ -73,10 +138,11 @@ __device__ void compact_row(const void* row, int Vp1, uint8_t* rec, uint64_t* ke
         double S = 0.0;
         if (in_regs) {
 #pragma unroll
-            for (int i = 0; i < kPerLane; ++i)
-                if (lane + 32 * i < Vp1) S += exp((double)v[i] - m);
+            for (int i = 0; i < NV; ++i)
+                if (v[i] > kNeg) S += exp((double)v[i] - m);  // exp(-inf) = 0: only finite logits count
+            if (lane == 0) S += exp((double)xb - m);
         } else {
-            for (int w = lane; w < Vp1; w += 32) S += exp((double)ld_x<BF16>(row, w) - m);
+            for (int w = lane; w < Vp1; w += 32) S += exp((double)ld_w(w) - m);
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
@@ -86,54 +152,78 @@ __device__ void compact_row(const void* row, int Vp1, uint8_t* rec, uint64_t* ke
         if constexpr (BF16) return (float)((double)x - lse);
         else return x;
     };
+    auto count_ge = [&](float th, int& mine) -> int {  // non-blank values >= th: this lane's, warp total
+        int c = 0;
+        if (in_regs) {
+            int c4[4] = {0, 0, 0, 0};  // independent partial sums (no serial add chain)
+#pragma unroll
+            for (int i = 0; i < NV; ++i) c4[i & 3] += v[i] >= th ? 1 : 0;
+            c = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+        } else {
+            for (int w = lane; w < blank; w += 32) c += ld_w(w) >= th ? 1 : 0;
+        }
+        mine = c;
+        return __reduce_add_sync(0xffffffffu, c);
+    };
 
     // band: the widest Δ in {16, 8, 4, 2, 1, 0} with at most kCmpList non-blank values >= mn - Δ
+    // (counts are monotone in Δ: a binary search over the six, <= 3 counting passes)
     float thr = INFINITY;
-    int n = 0;
+    int n = 0, h = 0;  // listed tokens: warp total, this lane's
     if (mn > kNeg) {
-        const float deltas[6] = {16.0f, 8.0f, 4.0f, 2.0f, 1.0f, 0.0f};
-        for (int k = 0; k < 6; ++k) {
-            const float th = __fsub_rn(mn, deltas[k]);
-            int c = 0;
-            if (in_regs) {
-#pragma unroll
-                for (int i = 0; i < kPerLane; ++i) c += (lane + 32 * i < blank && v[i] >= th) ? 1 : 0;
-            } else {
-                for (int w = lane; w < blank; w += 32) c += ld_x<BF16>(row, w) >= th ? 1 : 0;
-            }
-            c = __reduce_add_sync(0xffffffffu, c);
-            if (c <= kCmpList) { thr = th; n = c; break; }
+        int lo_i = 0, hi_i = 5;  // the smallest index (widest band) whose count fits; Δ = 16 >> index
+        while (lo_i <= hi_i) {
+            const int mid = (lo_i + hi_i) >> 1;
+            const float th = __fsub_rn(mn, mid == 5 ? 0.0f : (float)(16 >> mid));
+            int mine;
+            const int c = count_ge(th, mine);
+            if (c <= kCmpList) { thr = th; n = c; h = mine; hi_i = mid - 1; } else { lo_i = mid + 1; }
         }
     }
-    // collect the listed tokens (index order), then rank them by (D desc, token asc)
-    uint64_t mykey = 0;
+    // collect the listed tokens, then rank them by (value desc, token asc)
     if (n > 0) {
-        int base = 0;
-        auto take = [&](int w, float x) {
-            const bool hit = w < blank && x >= thr;
-            const unsigned bal = __ballot_sync(0xffffffffu, hit);
-            if (hit) {
-                const int q = base + __popc(bal & ((1u << lane) - 1u));
-                keys[q] = ((uint64_t)ord_of(x) << 32) | (uint64_t)(0xffffffffu - (uint32_t)w);
-            }
-            base += __popc(bal);
-        };
-        if (in_regs) {
+        int pos = h;  // exclusive prefix of the hit counts over the lanes
 #pragma unroll
-            for (int i = 0; i < kPerLane; ++i) take(lane + 32 * i, v[i]);
-        } else {
-            for (int w0 = 0; w0 < blank; w0 += 32) take(w0 + lane, w0 + lane < blank ? ld_x<BF16>(row, w0 + lane) : kNeg);
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pos, o);
+            if (lane >= o) pos += y;
+        }
+        pos -= h;
+        if (h) {
+            if (in_regs) {
+                // hit mask of this lane's elements, then one key per set bit
+                uint32_t hlo = 0, hhi = 0;
+#pragma unroll
+                for (int e = 0; e < NV; ++e) {
+                    if (e < 32) hlo |= (v[e] >= thr ? 1u : 0u) << e;
+                    else hhi |= (v[e] >= thr ? 1u : 0u) << (e - 32);
+                }
+                uint64_t hm = ((uint64_t)hhi << 32) | hlo;
+                while (hm) {
+                    const int e = __ffsll((long long)hm) - 1;
+                    hm &= hm - 1;
+                    const int w = tok_of(e / EPB, e % EPB);
+                    const float x = ld_w(w);  // an L1 hit (the row was just loaded)
+                    keys[pos++] = ((uint64_t)ord_of(x) << 32) | (uint64_t)(0xffffffffu - (uint32_t)w);
+                }
+            } else {
+                for (int w = lane; w < blank; w += 32) {
+                    const float x = ld_w(w);
+                    if (x >= thr) keys[pos++] = ((uint64_t)ord_of(x) << 32) | (uint64_t)(0xffffffffu - (uint32_t)w);
+                }
+            }
         }
         __syncwarp();
         if (lane < n) {
-            mykey = keys[lane];
-            int r = 0;
-            for (int j = 0; j < n; ++j) r += keys[j] > mykey ? 1 : 0;
+            const uint64_t mykey = keys[lane];
+            int r = 0, r2 = 0;
+            int j = 0;
+            for (; j + 1 < n; j += 2) { r += keys[j] > mykey ? 1 : 0; r2 += keys[j + 1] > mykey ? 1 : 0; }
+            if (j < n) r += keys[j] > mykey ? 1 : 0;
+            r += r2;
             const int w = (int)(0xffffffffu - (uint32_t)mykey);
-            float* val = (float*)(rec + 32);
-            uint16_t* tok = (uint16_t*)(rec + 160);
-            val[r] = dval(score_of(mykey));
-            tok[r] = (uint16_t)w;
+            ((float*)(rec + 32))[r] = dval(score_of(mykey));
+            ((uint16_t*)(rec + 160))[r] = (uint16_t)w;
         }
         __syncwarp();
     }
@@ -150,9 +240,10 @@ __device__ void compact_row(const void* row, int Vp1, uint8_t* rec, uint64_t* ke
 }
 
 template <bool BF16>
-__global__ void __launch_bounds__(32 * kWarps) frame_compact_kernel(const void* __restrict__ X, int64_t sb, int64_t stt,
+__global__ void __launch_bounds__(32 * kWarps, 3) frame_compact_kernel(const void* __restrict__ X, int64_t sb, int64_t stt,
                                                                    const int64_t* __restrict__ rowoff, int B, int T,
-                                                                   int Vp1, uint8_t* __restrict__ cmp) {
+                                                                   int Vp1, uint8_t* __restrict__ cmp, const char* lo,
+                                                                   const char* hi) {
     __shared__ uint64_t s_keys[kWarps][kCmpList];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t nrows = __ldg(&rowoff[B]);
@@ -161,19 +252,19 @@ __global__ void __launch_bounds__(32 * kWarps) frame_compact_kernel(const void* 
     for (int64_t c = (int64_t)blockIdx.x * kWarps + wid; c < nchunks; c += (int64_t)gridDim.x * kWarps) {
         int64_t r = c * kRowsPerWarp;
         // utterance of row r: the last b with rowoff[b] <= r (binary search, L1-resident)
-        int lo = 0, hi = B - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (__ldg(&rowoff[mid]) <= r) lo = mid; else hi = mid - 1;
+        int lo_b = 0, hi_b = B - 1;
+        while (lo_b < hi_b) {
+            const int mid = (lo_b + hi_b + 1) >> 1;
+            if (__ldg(&rowoff[mid]) <= r) lo_b = mid; else hi_b = mid - 1;
         }
-        int b = lo;
+        int b = lo_b;
         int64_t off = __ldg(&rowoff[b]), end = __ldg(&rowoff[b + 1]);
         const int64_t rend = min(nrows, r + kRowsPerWarp);
         for (; r < rend; ++r) {
             while (r >= end) { ++b; off = end; end = __ldg(&rowoff[b + 1]); }  // skips empty utterances
             const int t = (int)(r - off);
             const char* row = (const char*)X + ((int64_t)b * sb + (int64_t)t * stt) * esz;
-            compact_row<BF16>(row, Vp1, cmp + ((int64_t)b * T + t) * kCmpBytes, s_keys[wid], lane);
+            compact_row<BF16>(row, Vp1, cmp + ((int64_t)b * T + t) * kCmpBytes, s_keys[wid], lane, lo, hi);
         }
     }
 }
@@ -235,12 +326,17 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t max_chunks = ((int64_t)B * T + kRowsPerWarp - 1) / kRowsPerWarp;
     const int64_t want = (max_chunks + kWarps - 1) / kWarps;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * 16));
     cudaStream_t st = (cudaStream_t)stream;
+    // the tensor's byte range: no load leaves it (edge blocks of the first / last row are assembled
+    // element by element)
+    const size_t esz = bf16 ? 2 : 4;
+    const char* lo = (const char*)x;
+    const char* hi = lo + esz * ((size_t)(B - 1) * stride_b + (size_t)(T - 1) * stride_t + Vp1);
     if (bf16)
-        frame_compact_kernel<true><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp);
+        frame_compact_kernel<true><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi);
     else
-        frame_compact_kernel<false><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp);
+        frame_compact_kernel<false><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     return 0;

@@ -12,6 +12,8 @@
 namespace flexctc {
 
 void set_error(const std::string& msg);
+// name of the main kernel the last decode on this thread launched (flexctc_last_kernel)
+void set_kernel_name(const char* name);
 flexctc_status fail(flexctc_status st, const std::string& msg);
 
 // ---------------------------------------------------------------------------------------
@@ -65,12 +67,14 @@ struct BoostHost {
     int32_t V = 0, N = 0;
     std::vector<int32_t> tab;  // 2 ints per (node, token)
     std::vector<float> U, maxd;
+    std::vector<uint64_t> sig;  // per node: lm_sig_bit(a) of every token a with δ(u, a) != δ(root, a)
 };
 
 struct BoostDev {
     const int2* tab;
     const float* U;
     const float* maxd;
+    const unsigned long long* sig;  // exception signatures (BoostHost::sig)
     int32_t V;
     int64_t tab_bytes;
 };
@@ -131,7 +135,8 @@ struct DecodeParams {
     uint16_t* bp_label;   // [B][T][K]
     int32_t* align_ws;    // [B][T]
     float4* greedy_sum;   // [B][T] {d1, w1, d2, 0} frame summaries of the plain greedy path (K = 1)
-    uint8_t* cmp;         // [B][T][kCmpBytes] frame records (K <= 32 warp path), NULL otherwise
+    uint8_t* cmp;         // [B][T][kCmpBytes] frame records (K >= 2), NULL otherwise
+    int32_t use_cmp;      // the records were written by the compaction pass of this decode (CTA kernel)
     int64_t* rowoff;      // [B + 1] prefix of the clamped lengths (compaction pass rows)
     const uint16_t* logits;  // bf16 logits input of the warp path (log_probs unused), or NULL
     int32_t nch;
@@ -152,7 +157,9 @@ WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K);
 
 // launches (beam_kernel.cu; K = 1 goes to launch_greedy in greedy_kernel.cu)
 bool use_warp_path(const DecodeParams& p);  // K <= 32 warp path eligible (p.logits: bf16 input)
-int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
+// ev_start / ev_stop around the beam kernel, ev_cmp_start / ev_cmp_stop around the compaction pass
+int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err,
+                  void* ev_cmp_start = nullptr, void* ev_cmp_stop = nullptr);
 int launch_greedy(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
 // frame compaction pass (compact_kernel.cu): records of every valid row; rowoff by launch_rowoff
 int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, std::string& err);
@@ -161,6 +168,8 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
 // warp-per-utterance beam kernel (warp_beam_kernel.cu), K <= 32, after launch_compact
 int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev_start, void* ev_stop, std::string& err);
 size_t warp_beam_smem_per_warp(int Vp1, bool bf16, int nch);
+// helper mode of the warp path: one utterance per CTA, a beam warp + helper warps (B <= #SMs)
+bool warp_helper_mode(const DecodeParams& p, int nsm);
 // input side (input_kernel.cu): log-softmax of bf16 logits into a dense fp32 [B][T][Vp1] buffer
 // (frames [t0, t1) only; t1 = -1: every frame); preload_: force its module to load (see the .cu)
 int preload_log_softmax_bf16();

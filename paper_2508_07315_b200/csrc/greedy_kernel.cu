@@ -550,6 +550,7 @@ int launch_fused(const DecodeParams& p, cudaStream_t st, void* ev0, void* ev1, s
     const int grid = std::min((p.B + gw - 1) / gw, nsm * occ);
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
     kern<<<grid, 32 * gw, smem, st>>>(p, ringn);
+    set_kernel_name("greedy_fused_kernel");
     e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
@@ -576,6 +577,7 @@ int launch_greedy(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     if (plain) {
         greedy_chain_kernel<<<(p.B + 3) / 4, 128, 0, st>>>(p);
+        set_kernel_name("greedy_chain_kernel");
         e = cudaGetLastError();
         if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
         return 0;

@@ -49,9 +49,9 @@ class LmInfo(ctypes.Structure):
 
 EXPORTS = [
     "flexctc_last_error", "flexctc_version", "flexctc_lm_load", "flexctc_lm_free", "flexctc_lm_get_info",
-    "flexctc_lm_host_query", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
-    "flexctc_boost_num_nodes", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
-    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_decode_nbest", "flexctc_decode_logits_bf16", "flexctc_logits_workspace_bytes", "flexctc_set_profile_events", "flexctc_get_stats",
+    "flexctc_lm_host_query", "flexctc_lm_host_query_batch", "flexctc_lm_host_bound", "flexctc_boost_build", "flexctc_boost_free", "flexctc_boost_host_query",
+    "flexctc_boost_num_nodes", "flexctc_boost_host_query_batch", "flexctc_boost_host_signature", "flexctc_workspace_bytes", "flexctc_decode", "flexctc_check",
+    "flexctc_host_scratch_bytes", "flexctc_decode_host", "flexctc_host_streaming", "flexctc_decode_nbest", "flexctc_decode_logits_bf16", "flexctc_logits_workspace_bytes", "flexctc_set_profile_events", "flexctc_set_stage_events", "flexctc_last_kernel", "flexctc_get_stats",
     "flexctc_host_scratch_bytes_bf16", "flexctc_decode_host_bf16",
 ]
 STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_frames", "lm_rows_built",
@@ -87,6 +87,10 @@ def _declare(L: ctypes.CDLL) -> ctypes.CDLL:
     L.flexctc_boost_free.restype = None
     L.flexctc_boost_host_query.argtypes = [vp, i32, i32, P(f32), P(i32), P(f32)]
     L.flexctc_boost_num_nodes.argtypes = [vp, P(i32)]
+    L.flexctc_lm_host_query_batch.argtypes = [vp, i64, vp, vp, vp, vp]
+    L.flexctc_lm_host_bound.argtypes = [vp, i32, P(f32), P(f32)]
+    L.flexctc_boost_host_query_batch.argtypes = [vp, i64, vp, vp, vp, vp]
+    L.flexctc_boost_host_signature.argtypes = [vp, i32, P(ctypes.c_uint64)]
     L.flexctc_workspace_bytes.argtypes = [i32, i32, i32, P(Config)]
     L.flexctc_workspace_bytes.restype = sz
     L.flexctc_decode.argtypes = [vp, i64, i64, vp, i32, i32, i32, P(Config), vp, vp, vp, sz, vp,
@@ -110,6 +114,9 @@ def _declare(L: ctypes.CDLL) -> ctypes.CDLL:
     L.flexctc_host_streaming.restype = i32
     L.flexctc_set_profile_events.argtypes = [vp, vp]
     L.flexctc_set_profile_events.restype = None
+    L.flexctc_set_stage_events.argtypes = [ctypes.c_int32, vp, vp]
+    L.flexctc_set_stage_events.restype = ctypes.c_int
+    L.flexctc_last_kernel.restype = ctypes.c_char_p
     L.flexctc_get_stats.argtypes = [vp, vp, i32]
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if a declared symbol is missing
@@ -161,6 +168,22 @@ class LM:
         _check(lib.flexctc_lm_host_query(self.h, int(state), int(token), ctypes.byref(lp), ctypes.byref(nx)))
         return lp.value, nx.value
 
+    def host_query_batch(self, states, tokens):
+        """(logp f32[n], next i32[n]) for the (state, token) pairs."""
+        st = np.ascontiguousarray(states, dtype=np.int32)
+        tk = np.ascontiguousarray(tokens, dtype=np.int32)
+        lp = np.empty(st.shape[0], dtype=np.float32)
+        nx = np.empty(st.shape[0], dtype=np.int32)
+        _check(lib.flexctc_lm_host_query_batch(self.h, st.shape[0], st.ctypes.data, tk.ctypes.data, lp.ctypes.data,
+                                               nx.ctypes.data))
+        return lp, nx
+
+    def host_bound(self, state: int):
+        """(ub, LM.Final) of a state: the kernels' pre-prune bound ub >= max_w log P(w | state)."""
+        ub, eos = ctypes.c_float(), ctypes.c_float()
+        _check(lib.flexctc_lm_host_bound(self.h, int(state), ctypes.byref(ub), ctypes.byref(eos)))
+        return ub.value, eos.value
+
 
 class Boost:
     """flexctc_boost handle (flexctc_boost_build)."""
@@ -191,6 +214,21 @@ class Boost:
         _check(lib.flexctc_boost_host_query(self.h, int(node), int(token), ctypes.byref(d), ctypes.byref(nx),
                                             ctypes.byref(u)))
         return d.value, nx.value, u.value
+
+    def host_query_batch(self, nodes, tokens):
+        """(delta f32[n], next i32[n]) for the (node, token) pairs."""
+        nd = np.ascontiguousarray(nodes, dtype=np.int32)
+        tk = np.ascontiguousarray(tokens, dtype=np.int32)
+        d = np.empty(nd.shape[0], dtype=np.float32)
+        nx = np.empty(nd.shape[0], dtype=np.int32)
+        _check(lib.flexctc_boost_host_query_batch(self.h, nd.shape[0], nd.ctypes.data, tk.ctypes.data, d.ctypes.data,
+                                                  nx.ctypes.data))
+        return d, nx
+
+    def host_signature(self, node: int) -> int:
+        sg = ctypes.c_uint64()
+        _check(lib.flexctc_boost_host_signature(self.h, int(node), ctypes.byref(sg)))
+        return sg.value
 
 
 def _check_lengths(lengths, B: int, device=None, host: bool = False):
@@ -347,6 +385,18 @@ def set_profile_events(start=None, stop=None):
     """Record torch.cuda.Event `start`/`stop` around the beam kernel of later decode calls."""
     lib.flexctc_set_profile_events(ctypes.c_void_p(start.cuda_event) if start is not None else None,
                                    ctypes.c_void_p(stop.cuda_event) if stop is not None else None)
+
+
+def last_kernel() -> str:
+    """Name of the frame-loop kernel the last decode on this thread launched."""
+    return lib.flexctc_last_kernel().decode()
+
+
+def set_stage_events(stage: int, start=None, stop=None):
+    """Record torch.cuda.Event `start`/`stop` around a stage of later decode calls: 0 the beam
+    kernel, 1 the frame compaction pass (warp path only)."""
+    _check(lib.flexctc_set_stage_events(stage, ctypes.c_void_p(start.cuda_event) if start is not None else None,
+                                        ctypes.c_void_p(stop.cuda_event) if stop is not None else None))
 
 
 def stats(workspace: Workspace) -> dict:

@@ -41,7 +41,9 @@ def main():
     names = ["wait", "rb_rank", "pairs", "topk_update", "merge"]
     out = {"workload": a.workload, "frames": int(raw[0]), "evals": int(raw[3]), "tokens": int(raw[2]),
            "scan_frames": int(raw[4]), "pair_frames": int(raw[15]), "batches": int(raw[24]),
-           "row_loads": int(raw[25]), "lm_global": int(raw[26]), "lm_cached_row": int(raw[27])}
+           "row_loads": int(raw[25]), "lm_global": int(raw[26]), "lm_cached_row": int(raw[27]),
+           "jobs": int(raw[28]), "job_pairs": int(raw[29]), "job_candidates": int(raw[23]), "job_overflows": int(raw[22]), "lm_arc_cache": int(raw[21]),
+           "kernel": FX.last_kernel()}
     out["pair_detail_cycles_per_pair_frame"] = {k: round(int(raw[36 + i]) / max(1, int(raw[35])), 1) for i, k in
                                                 enumerate(["phaseA", "staging", "scan", "gather", "global_evals"])}
     out["pair_detail_cycles_per_pair_frame"]["pushes_with_keys"] = int(raw[41])

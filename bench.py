@@ -374,8 +374,8 @@ def run_flexctc(args):
     torch.cuda.synchronize()
     t_dec = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3        # s, whole decode per step summed
     t_kern = sum(e[2].elapsed_time(e[3]) for e in ev) / 1e3       # s, beam kernel only
-    t_cmp = sum(e[4].elapsed_time(e[5]) for e in ev) / 1e3  # s, compaction pass (0 when it did not run)
-    compacted = compacted or t_cmp > 1e-6
+    compacted = compacted or kernel_name.endswith("+records")  # CTA kernel reading the records
+    t_cmp = sum(e[4].elapsed_time(e[5]) for e in ev) / 1e3 if compacted else 0.0  # s, compaction pass
     t_dec_local = t_dec
     flags = F.check(ws)
     dstats = FX.stats(ws)  # device counters of the last timed decode

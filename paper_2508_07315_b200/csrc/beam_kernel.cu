@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const int RWS = RWC ? RWC : lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     constexpr bool plain = (FUS & 4) != 0;
     const bool ub_inf = plain ? false : (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
+    const bool use_cmp = FUS ? false : p.use_cmp != 0;  // records (FLEXCTC_CMP=1): generic variants only
     const int merge_mode = plain ? 0 : p.merge_mode;
     if (plain) nrow = 0;
     constexpr bool solo = SOLO;  // host: K <= 32 && NT >= 128 && R == kRing && !solo_off (>= 3 helper warps)
@@ -405,6 +406,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         return B;
     };
 
+    auto recof = [&](const Bank& B, int k) -> int* { return B.rec + (size_t)k * RWS; };  // slot k's LM record
     // exact candidate score of a non-blank, non-repeat token w from slot k (Eq. (1), R19 order)
     // With `row` (a cached LM row of the slot's state) the LM value comes from shared memory and
     // the next LM state is deferred (ln = -1) until the candidate is selected.
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         if (lm_on) {
             float lp;
             if (row) { lp = row[w]; ln = -1; }
-            else lp = lm_query<LMV>(p.lm, cur.rec + k * RWS, w, ln);
+            else lp = lm_query<LMV>(p.lm, recof(cur, k), w, ln);
             s = __fmaf_rn(p.alpha_lm, lp, s);
         }
         if (bt_on) { bn = e.x; s = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), s); }
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 if (r < L) {
                     wait_ready(p, r, ready);
                     load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
-                    if (p.use_cmp && ltid < kCmpBytes / 16)
+                    if (use_cmp && ltid < kCmpBytes / 16)
                         cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
                                    p.cmp + ((int64_t)b * p.T + r) * kCmpBytes + 16 * ltid);
                 }
@@ -483,7 +485,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 if (r < L) {
                     wait_ready(p, r, ready);
                     load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
-                    if (p.use_cmp && ltid < kCmpBytes / 16)
+                    if (use_cmp && ltid < kCmpBytes / 16)
                         cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
                                    p.cmp + ((int64_t)b * p.T + r) * kCmpBytes + 16 * ltid);
                 }
@@ -499,9 +501,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 // or, with records, the record's list (band <= 16 nats, <= 32 tokens) and floor
                 const int h = ltid;
                 helpers_sync(lnt);  // every helper's cp.async of row t (and record) has landed
-                const int rn = p.use_cmp ? ((const int*)rc_t)[2] : 0;
-                const float rfl = p.use_cmp ? ((const float*)rc_t)[1] : INFINITY;
-                if (p.use_cmp && !(rn == 0 && rfl == INFINITY)) {
+                const int rn = use_cmp ? ((const int*)rc_t)[2] : 0;
+                const float rfl = use_cmp ? ((const float*)rc_t)[1] : INFINITY;
+                if (use_cmp && !(rn == 0 && rfl == INFINITY)) {
                     const float* rv = (const float*)(rc_t + 32);
                     const uint16_t* rt = (const uint16_t*)(rc_t + 160);
                     if (h < rn) { s_list_tok[slot * kListCap + h] = rt[h]; s_list_d[slot * kListCap + h] = rv[h]; }
@@ -571,16 +573,16 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                 const int2 e = cur.bts[tid] == 0 ? btroot[lk] : __ldg(&p.bt.tab[(size_t)cur.bts[tid] * V + lk]);
                                 if (lm_on) {
                                     int nx;
-                                    srk = __fmaf_rn(p.alpha_lm, lm_query<LMV>(p.lm, cur.rec + tid * RWS, lk, nx), srk);
+                                    srk = __fmaf_rn(p.alpha_lm, lm_query<LMV>(p.lm, recof(cur, tid), lk, nx), srk);
                                 }
                                 srk = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), srk);
                             } else if (lm_on) {
                                 int nx;
-                                srk = __fmaf_rn(p.alpha_lm, lm_query<LMV>(p.lm, cur.rec + tid * RWS, lk, nx), srk);
+                                srk = __fmaf_rn(p.alpha_lm, lm_query<LMV>(p.lm, recof(cur, tid), lk, nx), srk);
                             }
                         }
                         float ub = p.beta;
-                        if (lm_on) ub += p.alpha_lm * __int_as_float(cur.rec[tid * RWS + 4]);
+                        if (lm_on) ub += p.alpha_lm * __int_as_float(recof(cur, tid)[4]);
                         if (bt_on) ub += p.alpha_bt * cur.btm[2 * tid];
                         ubk = ub_inf ? INFINITY : ub;
                     }
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 uint64_t best_tok = 0;
                 if (solo) {
                     best_tok = s_sum_key[slot];
-                } else if (p.use_cmp && !(((const int*)rc_t)[2] == 0 && ((const float*)rc_t)[1] == INFINITY)) {
+                } else if (use_cmp && !(((const int*)rc_t)[2] == 0 && ((const float*)rc_t)[1] == INFINITY)) {
                     // the record's best listed token (every unlisted one is <= floor <= it)
                     const int rn = ((const int*)rc_t)[2];
                     best_tok = rn > 0 ? make_key(((const float*)(rc_t + 32))[0], (uint32_t)((const uint16_t*)(rc_t + 160))[0])
@@ -649,8 +651,15 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 // enter the flat TopK, so it need not be scored; on blank-dominated
                 // frames this bound is far above fl(max - θ).
                 float thr = tau0;
-                {
-                    gsync(G);
+                // a frame whose best non-blank token cannot reach even tau0 <= thr needs no token
+                // filter: the K-th key (below) only tightens the filter of frames that scan
+                bool need_kth = true;
+                if (!stage_a && nalive > 0 && mxrb > kNeg) {
+                    const float mg0 = 1e-4f * (1.0f + fabsf(tau0) + fabsf(accmax) + fabsf(ubvmax));
+                    need_kth = dstar >= __fsub_rn(__fsub_rn(__fsub_rn(tau0, accmax), ubvmax), mg0);
+                }
+                gsync(G);
+                if (need_kth) {
                     const int nb = sc.nbuf;
                     if (nb >= K && nb <= 2 * G) thr = fmaxf(thr, score_of(kth_by_rank(sm.ckey, nb, K, sc, G)));
                 }
@@ -689,7 +698,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const bool scan_all = sc.scan;
             const int nalive = sc.nalive;
             const float ubvmax = sc.ubvmax;
-            if (scan_all && p.use_cmp && sc.dthr >= ((const float*)rc_t)[1]) {
+            if (scan_all && use_cmp && sc.dthr >= ((const float*)rc_t)[1]) {
                 // the record lists every token with D >= floor <= dthr: filter its list
                 const float dthr = sc.dthr;
                 const int excl = sc.excl;
@@ -768,7 +777,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     for (int a2 = tid; a2 < nalive; a2 += G4) {
                         const int k = sm.alive_idx[a2];
                         float ub = p.beta, ua = fabsf(p.beta), ubnl = p.beta;
-                        if (lm_on) { const float x = p.alpha_lm * __int_as_float(cur.rec[k * RWS + 4]); ub += x; ua += fabsf(x); }
+                        if (lm_on) { const float x = p.alpha_lm * __int_as_float(recof(cur, k)[4]); ub += x; ua += fabsf(x); }
                         if (bt_on) { const float x = p.alpha_bt * cur.btm[2 * k]; ub += x; ua += fabsf(x); ubnl += x; }
                         if (ub_inf) { ub = INFINITY; ubnl = INFINITY; }
                         s_pos[a2] = make_float4(cur.acc[k], ub, ua, __int_as_float(cur.last[k]));
@@ -923,7 +932,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         int ln = sm.slm[i];
                         const int bn = sm.sbt[i];
                         if (emit && ln < 0) {  // scored from a cached row: resolve the next LM state now
-                            lm_query<LMV>(p.lm, cur.rec + par * RWS, w, ln);
+                            lm_query<LMV>(p.lm, recof(cur, par), w, ln);
                             st[kDeferredNext] += 1;
                         }
                         if (emit) {  // new LM / BT states: fetch their records (latency overlaps phase 7)
@@ -1110,7 +1119,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         if (tid < K) {
             fs = cur.acc[tid];
             if (fs > kNeg) {
-                if (lm_on) fs = __fmaf_rn(p.alpha_lm, __int_as_float(cur.rec[tid * RWS + 5]), fs);
+                if (lm_on) fs = __fmaf_rn(p.alpha_lm, __int_as_float(recof(cur, tid)[5]), fs);
                 if (bt_on && p.retract) fs = __fmaf_rn(-p.alpha_bt, cur.btm[2 * tid + 1], fs);
             }
             sm.skey[tid] = (uint64_t)__float_as_uint(fs);
@@ -1362,16 +1371,16 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
             if (p.Vp1 == 1025) {
                 const bool plain = pl.nrow == 0 && p.merge_mode == 0 && !p.retract && p.alpha_lm >= 0.0f &&
                                    p.alpha_bt >= 0.0f;
-                if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // the north-star decode
+                if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // the north-star decode
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
-                else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && !p.use_bt && plain)  // LM only (c3)
+                else if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && !p.use_bt && plain)  // LM only (c3)
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 5><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
-                else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt)  // beam 16, 4-gram LM, boosting
+                else if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt)  // beam 16, 4-gram LM, boosting
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 3><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
-                else if (solo && p.K == 16 && p.use_lm && p.lm.RW == 16)  // beam 16 + 4-gram LM
+                else if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16)  // beam 16 + 4-gram LM
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo) ctc_beam_kernel<NT, LMV, true, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
-                else if (p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // K > 32, 4-gram LM, boosting (c5)
+                else if (!p.use_cmp && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // K > 32, 4-gram LM, boosting (c5)
                     ctc_beam_kernel<NT, LMV, false, 1025, 0, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else ctc_beam_kernel<NT, LMV, false, 1025><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 done = true;
@@ -1383,7 +1392,7 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
         (void)solo;
         bool done = false;
         if constexpr (NT == 64 && LMV == 2)  // throughput mode (B > 4 x #SMs) on the north-star decode
-            if (p.Vp1 == 1025 && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && pl.nrow == 0 &&
+            if (p.Vp1 == 1025 && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && pl.nrow == 0 &&
                 p.merge_mode == 0 && !p.retract && p.alpha_lm >= 0.0f && p.alpha_bt >= 0.0f) {
                 ctc_beam_kernel<NT, LMV, false, 1025, 16, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 done = true;
@@ -1393,7 +1402,7 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-    set_kernel_name("ctc_beam_kernel");
+    set_kernel_name(p.use_cmp ? "ctc_beam_kernel+records" : "ctc_beam_kernel");
     return 0;
 }
 

@@ -67,8 +67,8 @@ __device__ void compact_row(const void* row, int Vp1, uint8_t* rec, uint64_t* ke
     if (in_regs) {
         const uint64_t pol = policy_evict_first();
         const bool all_in = g >= lo && g + 16 * (size_t)nblk <= hi;  // every covering block inside the tensor
-#pragma unroll
         const uint32_t ninf = BF16 ? 0xff80ff80u : 0xff800000u;  // -inf in every element
+#pragma unroll
         for (int i = 0; i < kBlk<BF16>; ++i) {
             const int bi = lane + 32 * i;
             q[i] = make_uint4(ninf, ninf, ninf, ninf);
@@ -107,23 +107,20 @@ __device__ void compact_row(const void* row, int Vp1, uint8_t* rec, uint64_t* ke
     float v[NV];
     float mn = kNeg;  // max over non-blank tokens (NaN never wins)
     if (in_regs) {
-        // only the row's first block (elements before w = 0) and the blank's block (the blank and
-        // the bytes after it) hold elements that are not non-blank tokens; blocks past the row
-        // were filled with -inf
-        const int bl = (off + blank) / EPB, jb = off + blank - bl * EPB;  // the blank: block, element
+        float m4[4] = {kNeg, kNeg, kNeg, kNeg};  // independent partial maxima
 #pragma unroll
         for (int i = 0; i < kBlk<BF16>; ++i) {
-            const int bi = lane + 32 * i;
+            // valid elements j of block bi: [jlo, jhi) (interior blocks: all; the blank, the last
+            // element of the row, lies in the last block)
+            const int base = (lane + 32 * i) * EPB - off;
+            const int jlo = min(max(-base, 0), EPB), jhi = min(max(blank - base, 0), EPB);
 #pragma unroll
             for (int j = 0; j < EPB; ++j) {
                 const float x = elem<BF16>(q[i], j);
-                const bool out = (i == 0 && bi == 0 && j < off) || (bi == bl && j >= jb);
-                v[i * EPB + j] = out ? kNeg : x;
+                v[i * EPB + j] = (j >= jlo && j < jhi) ? x : kNeg;
+                m4[j & 3] = fmaxf(m4[j & 3], v[i * EPB + j]);
             }
         }
-        float m4[4] = {kNeg, kNeg, kNeg, kNeg};  // independent partial maxima
-#pragma unroll
-        for (int e = 0; e < NV; ++e) m4[e & 3] = fmaxf(m4[e & 3], v[e]);
         mn = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     } else {
         for (int w = lane; w < blank; w += 32) mn = fmaxf(mn, ld_w(w));

@@ -5,7 +5,8 @@
 Covers the beam-warp + helpers mode (K <= 32, LM + boosting), the whole-CTA mode (K = 64), the
 single-warp launch, the greedy kernels (plain and fused, K = 1; TMA bulk rows + mbarriers), the
 n-best output, the bf16-logits input pass and the streamed host path, on a few short utterances,
-and checks the results against the oracle."""
+and checks the results against the oracle. Round 2: the compaction pass, the warp kernel alone and
+in helper mode, and the CTA kernel reading compaction records."""
 import os
 import sys
 
@@ -78,8 +79,24 @@ def run_more():
               f"logits bf16 K={K}")
 
 
+def run_round2():
+    """Round 2 kernels: the compaction pass + warp kernel (alone and in helper mode: pair jobs,
+    boost signatures, LM arc cache, TMA rings), the CTA kernel reading compaction records (K = 16
+    beam-warp mode and K = 64 whole-CTA mode)."""
+    for env, K in ((dict(FLEXCTC_WARP="1", FLEXCTC_HELPERS="0"), 16), (dict(FLEXCTC_WARP="1", FLEXCTC_HELPERS="1"), 16),
+                   (dict(FLEXCTC_WARP="0", FLEXCTC_CMP="1"), 16), (dict(FLEXCTC_CMP="1"), 64)):
+        os.environ.update(env)
+        try:
+            run(K)
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+        print("  with", env)
+
+
 if __name__ == "__main__":
     run(16)
     run(64)
     run(16, nt=32)
     run_more()
+    run_round2()

@@ -323,7 +323,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
                                   flexctc_stream stream, int32_t* out_tokens, int32_t* out_num_tokens,
                                   float* out_scores, int32_t* out_timestamps, int32_t* out_alignment,
                                   const uint32_t* ready, int overread, int32_t nbest = 1,
-                                  const uint16_t* logits = nullptr) {
+                                  const uint16_t* logits = nullptr, int32_t wave = 0) {
     flexctc_status st = validate_cfg(cfg);
     if (st != FLEXCTC_OK) return st;
     if (nbest < 1 || nbest > cfg->beam) return fail(FLEXCTC_ERR_INVALID_ARG, "nbest must be in [1, beam]");
@@ -386,6 +386,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.out_tokens = out_tokens; p.out_num = out_num_tokens; p.out_scores = out_scores;
     p.out_ts = out_timestamps; p.out_align = out_alignment;
     p.ready = ready;
+    p.wave = ready ? wave : 0;
     p.overread = overread;
     p.nbest = nbest;
     std::string err;
@@ -475,7 +476,7 @@ flexctc_status flexctc_check(const void* workspace, uint32_t* device_flags) {
 
 size_t flexctc_host_scratch_bytes(int32_t B, int32_t T, int32_t Vp1, const flexctc_config* cfg) {
     if (!cfg || B < 0 || T < 0 || Vp1 < 2 || cfg->beam < 1) return 0;
-    size_t s = align256((size_t)B * T * Vp1 * 4 + 16) + align256((size_t)B * 4) + 256;
+    size_t s = align256((size_t)B * T * Vp1 * 4 + 16) + align256((size_t)B * 4) * 2 + 256;  // D, lengths, LPT order
     s += align256((size_t)B * T * 4) * 2 + align256((size_t)B * 4) * 2;
     s += workspace_layout(B, T, cfg->beam).total;
     return s;
@@ -582,6 +583,7 @@ flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* le
     size_t o = 0;
     float* dD = (float*)(d + o); o += align256((size_t)B * T * Vp1 * 4 + 16);  // + 16 B slack (overread)
     int32_t* dL = (int32_t*)(d + o); o += align256((size_t)B * 4);
+    int32_t* dOrd = (int32_t*)(d + o); o += align256((size_t)B * 4);  // LPT order (ragged streamed input)
     int32_t* dTok = (int32_t*)(d + o); o += align256((size_t)B * T * 4);
     int32_t* dTs = (int32_t*)(d + o); o += align256((size_t)B * T * 4);
     int32_t* dN = (int32_t*)(d + o); o += align256((size_t)B * 4);
@@ -607,9 +609,40 @@ flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* le
     std::string err;
     if (streamed && bf16 && preload_log_softmax_bf16())
         return fail(FLEXCTC_ERR_CUDA, "cannot load the bf16 normalisation kernel");
+    // Ragged batches: frames of the utterances still live in a chunk are gathered by a small kernel
+    // that reads the caller's buffer over PCIe when it is pinned (device-mapped); one 2D copy per
+    // run of live utterances otherwise (many copy calls for LibriSpeech-shaped lengths)
+    const char* x_dev = nullptr;
+    if (streamed) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, x_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
+            ((uintptr_t)pa.devicePointer & 15) == 0)  // same 16-B alignment as the device copy
+            x_dev = (const char*)pa.devicePointer;
+        cudaGetLastError();
+        if (x_dev && preload_gather_rows()) x_dev = nullptr;
+    }
+    // Ragged fp32 input from a device-mapped buffer: the first wave of utterances (LPT positions
+    // < #SMs, the ones the persistent kernel starts with) is sent frame-major, the rest whole in
+    // LPT order, exactly when the kernel's work queue reaches them (a frame-major stream over all
+    // utterances would feed utterances that start much later and starve the first wave).
+    int Lmin = T;
+    for (int b = 0; b < B; ++b) Lmin = std::min(Lmin, std::min(std::max(lengths_host[b], 0), T));
+    int wave = 0;
+    std::vector<int32_t> ord;
+    if (streamed && x_dev && !bf16 && Lmin < T && B > nsm) {
+        wave = nsm;
+        ord.resize(B);
+        for (int b = 0; b < B; ++b) ord[b] = b;
+        if (B <= 16384)  // order_kernel's rule: length desc, ties to the lower index (identity above)
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int c) {
+                return std::min(std::max(lengths_host[a], 0), T) > std::min(std::max(lengths_host[c], 0), T);
+            });
+        e = cudaMemcpyAsync(dOrd, ord.data(), (size_t)B * 4, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+    }
     if (streamed) {
         ready = (uint32_t*)((char*)ws + wl.flags + 64 + 8 * kStatsWords);
-        e = cudaMemsetAsync(ready, 0, 4, s);
+        e = cudaMemsetAsync(ready, 0, 8, s);
         if (e == cudaSuccess) e = cudaEventRecord(g_host.ev_a, s);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(g_host.copy, g_host.ev_a, 0);
         if (e != cudaSuccess) return cuda_fail(e, "stream setup");
@@ -622,7 +655,8 @@ flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* le
         }
     }
     st = decode_impl(dD, (int64_t)T * Vp1, Vp1, dL, B, T, Vp1, cfg, lm, boost, ws, wsb, stream, dTok, dN, dS,
-                     out_timestamps ? dTs : nullptr, nullptr, ready, 1);
+                     out_timestamps ? dTs : nullptr, nullptr, ready, 1, 1, nullptr, wave);
+    // (the pageable `ord` upload above returned once staged: the vector may go)
     if (st != FLEXCTC_OK) {
         if (streamed) cudaStreamSynchronize(s);
         return st;
@@ -631,15 +665,24 @@ flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* le
         // chunk c: frames [t0, t1) of every utterance with L_b > t0 (rows of one utterance are
         // contiguous), [bf16: normalised into dD], then ready = t1
         const size_t row = (size_t)Vp1 * esz;
-        int Lmin = T;
-        for (int b = 0; b < B; ++b) Lmin = std::min(Lmin, std::min(std::max(lengths_host[b], 0), T));
         const char* xh = (const char*)x_host;
         int t0 = 0;
-        for (int t1 : chunk_ends(T)) {
-            if (t1 <= Lmin) {  // every utterance needs the whole chunk: one 2D copy
+        int Tw = T;  // frames of the first wave
+        if (wave) {
+            Tw = 0;
+            for (int u = 0; u < wave; ++u) Tw = std::max(Tw, std::min(std::max(lengths_host[ord[u]], 0), T));
+        }
+        for (int t1 : chunk_ends(Tw)) {
+            if (t1 <= Lmin && !wave) {  // every utterance needs the whole chunk: one 2D copy
                 e = cudaMemcpy2DAsync(dIn + (size_t)t0 * row, (size_t)T * row, xh + (size_t)t0 * row,
                                       (size_t)T * row, row * (size_t)(t1 - t0), (size_t)B, cudaMemcpyHostToDevice,
                                       g_host.copy);
+            } else if (x_dev) {
+                // ragged, pinned: one gather launch copies the chunk's valid frames of every
+                // utterance (of the first wave when waved)
+                if (launch_gather_rows(x_dev, dIn, dL, wave ? dOrd : nullptr, wave ? wave : B, T, (int64_t)row, t0, t1,
+                                       32, (void*)g_host.copy, err))
+                    e = cudaErrorUnknown;
             } else {
                 // ragged: one 2D copy of the whole chunk per maximal run of consecutive utterances
                 // with L_b > t0 (an utterance ending inside the chunk also gets its padding rows
@@ -663,6 +706,15 @@ flexctc_status decode_host_impl(const void* x_host, bool bf16, const int32_t* le
                 e = cudaErrorUnknown;
             if (e != cudaSuccess) break;
             t0 = t1;
+        }
+        // the later utterances whole, in LPT order, in growing groups; ready[1] = how many landed
+        for (int u0 = wave, g = 4; wave && u0 < B && e == cudaSuccess; u0 += g, g = std::min(64, 2 * g)) {
+            const int u1 = std::min(B, u0 + g);
+            if (launch_gather_rows(x_dev, dIn, dL, dOrd + u0, u1 - u0, T, (int64_t)row, 0, T, 32, (void*)g_host.copy, err))
+                e = cudaErrorUnknown;
+            if (e == cudaSuccess && g_host.write32((CUstream)g_host.copy, (CUdeviceptr)(ready + 1),
+                                                   (cuuint32_t)(u1 - wave), 0) != CUDA_SUCCESS)
+                e = cudaErrorUnknown;
         }
         if (e == cudaSuccess) e = cudaEventRecord(g_host.ev_b, g_host.copy);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, g_host.ev_b, 0);

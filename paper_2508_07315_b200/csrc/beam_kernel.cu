@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         const int b = p.order[u];
         const int L = p.len_c[b];
         const float* Db = p.log_probs + (int64_t)b * p.stride_b;
+        ready = 0;  // streamed input: what this thread has seen landed, per utterance
         const int64_t bp_base = (int64_t)b * p.T * K;  // backpointers of this utterance
 
         // ------------------------------------------------------------ init (Alg. 1)
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         if (!solo || helper)
             for (int r = 0; r < pf; ++r) {  // prologue
                 if (r < L) {
-                    wait_ready(p, r, ready);
+                    wait_ready(p, u, r, ready);
                     load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
                     if (use_cmp && ltid < kCmpBytes / 16)
                         cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             if (!solo || helper) {
                 const int r = t + pf;
                 if (r < L) {
-                    wait_ready(p, r, ready);
+                    wait_ready(p, u, r, ready);
                     load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
                     if (use_cmp && ltid < kCmpBytes / 16)
                         cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
@@ -1478,13 +1479,12 @@ bool use_warp_path(const DecodeParams& p) {
     if (e && e[0] == '0') return false;
     if (!(e && e[0] == '1')) {
         // Up to 4 x #SMs utterances the persistent CTA kernel (2-8 warps per utterance, up to 592
-        // in flight) has the shorter frame step (the warp kernel's helper mode, opt-in, measured
-        // slower at c4); beyond, the warp kernel's one warp per utterance packs more utterances
-        // per SM (tools/policy_sweep.py, profiles/r2/policy_*.jsonl)
+        // in flight) has the shorter frame step; beyond, the warp kernel's one warp per utterance
+        // packs more utterances per SM (tools/policy_sweep.py, profiles/r2/policy_*.jsonl)
         int dev = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (p.B <= 4 * nsm && !warp_helper_mode(p, nsm)) return false;
+        if (p.B <= 4 * nsm) return false;
     }
     const size_t per = warp_beam_smem_per_warp(p.Vp1, p.logits != nullptr, p.nch);
     return per + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0) <= 200 * 1024;

@@ -137,16 +137,21 @@ __device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1,
     if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
 }
 
-// Streamed input (flexctc_decode_host): wait until frame r of every utterance has landed.
-// `ready` caches the last value seen by this thread (frames only ever become ready). A 10 s
-// watchdog flags FLEXCTC_FLAG_STREAM_TIMEOUT instead of hanging the device.
-__device__ __forceinline__ void wait_ready(const DecodeParams& p, int r, int& ready) {
+// Streamed input (flexctc_decode_host): wait until frame r of the utterance at LPT position u has
+// landed. First wave (u < p.wave, or p.wave = 0): ready[0] > r (frames sent frame-major); later
+// utterances: ready[1] > u - p.wave (sent whole, in LPT order). `ready` caches what this thread
+// has seen for the current utterance (reset per utterance). A 10 s watchdog flags
+// FLEXCTC_FLAG_STREAM_TIMEOUT instead of hanging the device.
+__device__ __forceinline__ void wait_ready(const DecodeParams& p, int u, int r, int& ready) {
     if (!p.ready || r < ready) return;
+    const bool whole = p.wave > 0 && u >= p.wave;
+    const uint32_t* word = p.ready + (whole ? 1 : 0);
+    const int need = whole ? u - p.wave : r;
     const long long t0 = clock64();
     uint32_t v;
     for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready) : "memory");
-        if ((int)v > r) break;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(word) : "memory");
+        if ((int)v > need) { if (whole) v = 0x7fffffffu; break; }
         if (clock64() - t0 > 20000000000ll) {
             atomicOr(p.flags, FLEXCTC_FLAG_STREAM_TIMEOUT);
             v = 0x7fffffffu;

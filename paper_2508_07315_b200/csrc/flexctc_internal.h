@@ -119,6 +119,10 @@ struct DecodeParams {
     // streamed input (flexctc_decode_host): frames [0, *ready) of every utterance have landed in
     // log_probs; the row loaders poll it (ld.acquire) before issuing a row. NULL = all resident.
     const uint32_t* ready;
+    // wave > 0 (ragged host input): ready[0] counts the frames landed for the utterances at LPT
+    // positions < wave (sent frame-major); ready[1] counts the utterances at positions wave, wave+1,
+    // ... that have landed whole (sent in LPT order after the first wave)
+    int32_t wave;
     // log_probs is a library-owned buffer with >= 16 B of slack on both sides of every row, so
     // rows are copied as whole 16-B blocks (no 4-B .ca copies that could cache stale sectors
     // while a chunk is still in flight)
@@ -168,11 +172,15 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
 // warp-per-utterance beam kernel (warp_beam_kernel.cu), K <= 32, after launch_compact
 int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev_start, void* ev_stop, std::string& err);
 size_t warp_beam_smem_per_warp(int Vp1, bool bf16, int nch);
-// helper mode of the warp path: one utterance per CTA, a beam warp + helper warps (B <= #SMs)
-bool warp_helper_mode(const DecodeParams& p, int nsm);
 // input side (input_kernel.cu): log-softmax of bf16 logits into a dense fp32 [B][T][Vp1] buffer
 // (frames [t0, t1) only; t1 = -1: every frame); preload_: force its module to load (see the .cu)
 int preload_log_softmax_bf16();
+// streamed host input: copy frames [t0, min(L_b, t1)) of every utterance from a device-mapped
+// pinned host buffer to the device copy (same layout); preload_: load the module before the
+// persistent kernel starts (a lazy module load would wait for it)
+int preload_gather_rows();
+int launch_gather_rows(const void* src_dev, void* dst, const int32_t* lengths, const int32_t* order, int n, int T,
+                       int64_t row_bytes, int t0, int t1, int ctas, void* stream, std::string& err);
 int launch_log_softmax_bf16(const uint16_t* x, int64_t stride_b, int64_t stride_t, const int32_t* lengths, int B,
                             int T, int Vp1, float* out, void* stream, std::string& err, int t0 = 0, int t1 = -1);
 

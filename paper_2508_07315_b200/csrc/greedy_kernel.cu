@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
         // frame rows: one TMA bulk copy per row (lane 0), ringn - 1 rows ahead
         int nissued = 0, ncons = 0;
         for (int r = 0; r < ringn - 1 && r < L; ++r) {
-            wait_ready(p, r, ready);
+            wait_ready(p, 0, r, ready);
             bulk_row(ring + (size_t)r * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, &bar[r], lo, hi, lane);
         }
         nissued = min(ringn - 1, L);
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(32 * kGW) greedy_fused_kernel(const DecodePara
                     // every lane's reads of this slot (frame t - 1) precede lane 0's proxy fence and the
                     // async-proxy (TMA) write that reuses it
                     __syncwarp();
-                    wait_ready(p, r, ready);
+                    wait_ready(p, 0, r, ready);
                     bulk_row(ring + (size_t)(r & (ringn - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1,
                              &bar[r & (ringn - 1)], lo, hi, lane);
                     nissued = r + 1;

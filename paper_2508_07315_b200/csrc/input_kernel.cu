@@ -10,6 +10,7 @@
 // agree except at a rounding boundary.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 
@@ -75,7 +76,58 @@ __global__ void __launch_bounds__(32 * kRows) log_softmax_bf16_kernel(const uint
     for (int w = lane; w < Vp1; w += 32) d[w] = (float)((double)bf16f(x[w]) - lse);
 }
 
+// Streamed host input (flexctc_decode_host): frames [t0, min(L_b, t1)) of n utterances (b =
+// order[i], or i) from the
+// caller's pinned host buffer (device-mapped: the loads travel over PCIe) to the same offsets of
+// the device copy. One CTA per utterance in turn; the byte range of an utterance's chunk is
+// contiguous and has the same alignment on both sides (both bases are 16-B aligned and the
+// layouts are identical), so it moves as 16-B loads/stores with <= 15 bytes each side done by
+// bytes. A few CTAs reach the PCIe rate (~51 GB/s measured with 16 x 1024 threads,
+// tools/micro/zc.cu), so the gather runs next to the persistent beam kernel.
+__global__ void __launch_bounds__(256) gather_rows_kernel(const char* __restrict__ src, char* __restrict__ dst,
+                                                         const int32_t* __restrict__ lengths,
+                                                         const int32_t* __restrict__ order, int n, int T,
+                                                         int64_t row_bytes, int t0, int t1) {
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const int b = order ? __ldg(&order[i]) : i;
+        const int L = min(max(__ldg(&lengths[b]), 0), T);
+        const int te = min(L, t1);
+        if (te <= t0) continue;
+        const int64_t lo = ((int64_t)b * T + t0) * row_bytes, hi = ((int64_t)b * T + te) * row_bytes;
+        const int64_t a0 = (lo + 15) & ~(int64_t)15, a1 = hi & ~(int64_t)15;
+        if (a0 >= a1) {
+            for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) dst[i] = src[i];
+            continue;
+        }
+        for (int64_t i = lo + threadIdx.x; i < a0; i += blockDim.x) dst[i] = src[i];
+        for (int64_t i = a1 + threadIdx.x; i < hi; i += blockDim.x) dst[i] = src[i];
+        const uint4* s4 = (const uint4*)(src + a0);
+        uint4* d4 = (uint4*)(dst + a0);
+        const int64_t n4 = (a1 - a0) >> 4;
+        for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) {
+            uint4 v;
+            asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(s4 + i));
+            d4[i] = v;
+        }
+    }
+}
+
 }  // namespace
+
+int preload_gather_rows() {
+    cudaFuncAttributes a{};
+    return cudaFuncGetAttributes(&a, gather_rows_kernel) == cudaSuccess ? 0 : 1;
+}
+
+int launch_gather_rows(const void* src_dev, void* dst, const int32_t* lengths, const int32_t* order, int n, int T,
+                       int64_t row_bytes, int t0, int t1, int ctas, void* stream, std::string& err) {
+    if (n <= 0 || t1 <= t0) return 0;
+    gather_rows_kernel<<<std::max(1, std::min(n, ctas)), 256, 0, (cudaStream_t)stream>>>(
+        (const char*)src_dev, (char*)dst, lengths, order, n, T, row_bytes, t0, t1);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
+    return 0;
+}
 
 // CUDA loads a kernel's module lazily on its first launch, and that load waits for running
 // kernels: launched next to a persistent kernel that waits for its output, the first launch

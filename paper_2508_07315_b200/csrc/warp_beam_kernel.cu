@@ -51,21 +51,13 @@ constexpr int kWBMax = 8;      // warps (utterances in flight) per CTA, at most
 constexpr int kWRing = 4;      // frames in flight per warp (power of two)
 constexpr int kCandCap = 128;  // candidate keys per warp
 constexpr int kPairCap = 512;  // gathered (slot, token) pairs per chunk
-// helper mode (NHW > 0 helper warps next to the beam warp, one utterance per CTA): the pair
-// phase of a frame is one parallel job of the whole CTA over at most kJobPairs pairs
-constexpr int kJobPairs = 1024;
-constexpr int kHelpCandCap = kCandCap + kJobPairs;
 
 struct WLayout {
-    size_t rowslot, ring_rows, ring_recs, bars, ckey, cln, cbn, slots, pack, pairs, tlist, endslot, rmeta, abar, arcs, rows,
-        total;
+    size_t rowslot, ring_rows, ring_recs, bars, ckey, cln, cbn, slots, pairs, tlist, endslot, rmeta, rows, total;
 };
 
-// nrow: NGPU-LM dense level-1 rows cached per warp (tag = row index u, loaded by TMA);
-// candcap: candidate buffer entries (kCandCap, or kHelpCandCap in helper mode)
-// nae: LM arc-cache entries (helper mode: 2K; each holds <= kACap arcs of both arc levels)
-constexpr int kACap = 16;
-__host__ __device__ inline WLayout wlayout(int Vp1, int esz, int nch, int nrow, int candcap = kCandCap, int nae = 0) {
+// nrow: NGPU-LM dense level-1 rows cached per warp (tag = row index u, loaded by TMA)
+__host__ __device__ inline WLayout wlayout(int Vp1, int esz, int nch, int nrow) {
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
     WLayout L{};
     L.rowslot = al((size_t)Vp1 * esz + 30);  // covering 16-B blocks of a row at any alignment
@@ -73,18 +65,14 @@ __host__ __device__ inline WLayout wlayout(int Vp1, int esz, int nch, int nrow, 
     L.ring_rows = o; o += kWRing * L.rowslot;
     L.ring_recs = o; o += kWRing * (size_t)kCmpBytes;
     L.bars = o; o += al(8 * kWRing);
-    L.ckey = o; o += 8 * ((size_t)candcap + 2);  // + a zero sentinel for the paired loads of rank_pass
-    L.cln = o; o += 4 * (size_t)candcap;
-    L.cbn = o; o += 4 * (size_t)candcap;
-    L.slots = o; o += 24 * 32 * 4;  // acc ub ua last lms bts sel rs ord rsort row cumu cumr sglo sghi bU bsglo bsghi
-                                    // aent adeg acum0 acum1 (2 spare)
-    L.pack = o; o += 16 * 32;
+    L.ckey = o; o += 8 * (kCandCap + 2);  // + a zero sentinel for the paired loads of rank_pass
+    L.cln = o; o += 4 * kCandCap;
+    L.cbn = o; o += 4 * kCandCap;
+    L.slots = o; o += 20 * 32 * 4;  // acc ub ua last lms bts sel rs ord rsort row cumu cumr sglo sghi bU bsglo bsghi (2 spare)
     L.pairs = o; o += 4 * kPairCap;
     L.tlist = o; o += al(2 * (size_t)Vp1);
     L.endslot = o; o += al(4 * (size_t)nch);
-    L.rmeta = o; o += al(12 * (size_t)nrow) + al(8 * (size_t)nrow);  // tag, last use, load frame; mbarrier per cached row
-    L.abar = o; o += al(8 * (size_t)nae);
-    L.arcs = o; o += (size_t)nae * 2 * kACap * 16;
+    L.rmeta = o; o += al(16 * (size_t)nrow);  // tag, last use, mbarrier per cached row
     L.rows = o; o += (size_t)nrow * (size_t)(Vp1 - 1) * 8;
     L.total = al(o);
     return L;
@@ -96,36 +84,13 @@ __device__ __forceinline__ float ord_inv(uint32_t o) {  // inverse of ord_of
 }
 __device__ __forceinline__ int shi(int v, int s) { return __shfl_sync(0xffffffffu, v, s); }
 
-// The pair job of helper mode: posted by the beam warp in shared memory, run by the whole CTA.
-struct PairJob {
-    int cmd;                     // 1: score the pairs of this frame, 2: no more utterances
-    float thr, dt, uamax;        // running threshold, token filter D >= dt, max |ub terms|
-    int jA, m0, scan, nalive;    // listed tokens [jA, m0); scan the row for unlisted tokens
-    int np, nc;                  // gathered pairs (may exceed kJobPairs: overflow), candidates
-    int wA;                      // token scored from every slot by the beam warp (-1: none)
-    int t;                       // the frame
-    uint32_t kmax;               // best candidate score so far (ord_of image)
-    uint32_t rph;                // parities of the cached dense rows' latest loads
-    unsigned long long aph;      // parities of the arc-cache entries' latest loads
-    float xthr;                  // listed iff the raw value >= xthr
-    const unsigned char* rc;     // the frame record and row in the ring
-    const unsigned char* rowb;
-    double lse;
-};
-
-__device__ __forceinline__ void job_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
-
-// NHW: helper warps per CTA (0: up to kWBMax independent beam warps per CTA; > 0: warp 0 is the
-// beam warp of the CTA's utterance and warps 1..NHW join it for the pair phase of a frame)
-template <int LMV, bool BF16, int NHW>
-__global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kernel(const DecodeParams p, const int nrow) {
+template <int LMV, bool BF16>
+__global__ void __launch_bounds__(32 * kWBMax) warp_beam_kernel(const DecodeParams p, const int nrow) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = NHW ? 0 : threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int K = p.K, Vp1 = p.Vp1, blank = Vp1 - 1, V = Vp1 - 1;
     constexpr int esz = BF16 ? 2 : 4;
-    constexpr int NT = 32 * (NHW + 1);  // threads of a pair job
-    const WLayout WL = wlayout(Vp1, esz, p.nch, nrow, NHW ? kHelpCandCap : kCandCap, NHW ? 2 * p.K : 0);
-    __shared__ PairJob jb;
+    const WLayout WL = wlayout(Vp1, esz, p.nch, nrow);
     unsigned char* ws = smem_raw + (size_t)wid * WL.total;
     unsigned char* ring_rows = ws + WL.ring_rows;
     unsigned char* ring_recs = ws + WL.ring_recs;
@@ -148,44 +113,31 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
     float* s_cumr = s_acc + 384;
     uint32_t* s_sglo = (uint32_t*)(s_acc + 416);
     uint32_t* s_sghi = (uint32_t*)(s_acc + 448);
-    float4* s_pack = (float4*)(ws + WL.pack);   // helper mode: live slots in reach order {acc, ub, ua, last << 8 | slot}
-    float* s_bU = s_acc + 480;                  // boost: U of the slot's node
+    float* s_bU = s_acc + 480;                     // boost: U of the slot's node
     uint32_t* s_bsglo = (uint32_t*)(s_acc + 512);  // boost: exception signature of the slot's node
     uint32_t* s_bsghi = (uint32_t*)(s_acc + 544);
-    int* s_aent = (int*)(s_acc + 576);            // helper mode: the slot's arc-cache entry (-1: none)
-    int* s_adeg = (int*)(s_acc + 608);            // its levels: n | deg0 << 8 | deg1 << 16 (degrees capped at 255)
-    float* s_acum0 = s_acc + 640;                 // cumulative backoffs of arc levels 0 and 1
-    float* s_acum1 = s_acc + 672;
-    int* s_lmu = (int*)(s_acc + 704);             // the slot's level-1 row index (dense row)
-    uint64_t* abar = (uint64_t*)(ws + WL.abar);   // arc-cache mbarriers
-    int4* acache = (int4*)(ws + WL.arcs);         // [nae][2][kACap] arcs {token, logp, next, 0}
-    const int nae = NHW ? 2 * K : 0;
     int* rtag = (int*)(ws + WL.rmeta);
     int* ruse = rtag + nrow;
-    int* rload = ruse + nrow;  // frame at which the row's latest load was issued
-    uint64_t* rbar = (uint64_t*)(ws + WL.rmeta + ((12 * (size_t)nrow + 15) & ~(size_t)15));
+    uint64_t* rbar = (uint64_t*)(ws + WL.rmeta + 8 * (size_t)nrow);
     const int2* rows = (const int2*)(ws + WL.rows);
     uint32_t* s_pairs = (uint32_t*)(ws + WL.pairs);
     uint16_t* tlist = (uint16_t*)(ws + WL.tlist);
     int* endslot = (int*)(ws + WL.endslot);
-    int2* btroot = (int2*)(smem_raw + (size_t)(NHW ? 1 : blockDim.x >> 5) * WL.total);
-    uint2* jpairs = (uint2*)((unsigned char*)btroot + (p.use_bt ? 8 * (size_t)V : 0));  // [kJobPairs] (NHW > 0)
+    int2* btroot = (int2*)(smem_raw + (size_t)(blockDim.x >> 5) * WL.total);
 
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
     const bool ub_inf = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
     const int RW4 = lm_on ? p.lm.RW / 4 : 0;
     if (bt_on)
         for (int w = threadIdx.x; w < V; w += blockDim.x) btroot[w] = __ldg(&p.bt.tab[w]);
-    if (NHW ? threadIdx.x == 0 : lane == 0) {
+    if (lane == 0) {
         for (int i = 0; i < kWRing; ++i) mbar_init(&bar[i], 1);
-        for (int i = 0; i < nrow; ++i) { mbar_init(&rbar[i], 1); rtag[i] = -1; ruse[i] = -1; rload[i] = -1; }
-        for (int i = 0; i < (NHW ? 2 * K : 0); ++i) mbar_init(&abar[i], 1);
+        for (int i = 0; i < nrow; ++i) { mbar_init(&rbar[i], 1); rtag[i] = -1; ruse[i] = -1; }
         fence_mbar_init();
     }
     __syncthreads();
     uint32_t ph = 0;  // expected parity of each ring slot's next completion
     uint32_t rph = 0xffffffffu;  // parity of the latest load of each cached row (uniform over the warp)
-    unsigned long long aph = ~0ull;  // parity of the latest load of each arc-cache entry (uniform)
     const char* xbase = BF16 ? (const char*)p.logits : (const char*)p.log_probs;
     const char* lo = xbase;
     const char* hi = xbase + (int64_t)esz * ((int64_t)(p.B - 1) * p.stride_b + (int64_t)(p.T - 1) * p.stride_t + Vp1);
@@ -196,208 +148,7 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
     long long tq = 0;
 #endif
     unsigned long long st_frames = 0, st_alive = 0, st_listed = 0, st_eval = 0, st_scan = 0, st_pairfr = 0;
-    unsigned long long st_batch = 0, st_lmg = 0, st_lmr = 0, st_rowld = 0, st_lmc = 0;
-    unsigned long long st_jobs = 0, st_jpairs = 0, st_jcands = 0;  // helper mode: jobs, their pairs, candidates
-    unsigned long long st_jover = 0;  // jobs handed back to the single-warp path (too many pairs)
-    // exact score of token w (log-prob d) from a slot given by its fields; key 0 if < th
-    // (rp: parities of the cached dense rows' latest loads)
-    // Boost: from a non-root node u, a token outside u's exception signature has δ(u, w) =
-    // δ(root, w) and delta = fl(delta(root, w) - U(u)) exactly (boost_build.cpp): the root row
-    // in shared memory serves it; signature hits read the transition table.
-    // LM (lm_query's result, same fp32 operations): a token outside the state's arc signature is
-    // decided by the dense level-1 row (cached in shared memory when lrow_k >= 0); a signature hit
-    // searches the state's arc levels, from the arc cache (helper mode, aent_k >= 0, every level
-    // <= kACap arcs) or the global sorted arcs.
-    auto eval = [&](float acc_k, float d, int w, int lms_k, int bts_k, int lrow_k, float cumu_k, float cumr_k,
-                    uint32_t sglo_k, uint32_t sghi_k, float bU_k, uint32_t bsglo_k, uint32_t bsghi_k, int lmu_k,
-                    int aent_k, int adeg_k, float acum0_k, float acum1_k, int k, int& ln, int& bn, float th,
-                    uint32_t rp, unsigned long long ap) -> uint64_t {
-        float sx = __fadd_rn(__fadd_rn(acc_k, d), p.beta);
-        ln = lms_k;
-        bn = bts_k;
-        const int sbit = lm_sig_bit(w);
-        int2 e = make_int2(0, 0);
-        if (bt_on) {
-            if (bn == 0) {
-                e = btroot[w];
-            } else if (((sbit < 32 ? bsglo_k : bsghi_k) >> (sbit & 31)) & 1u) {
-                e = __ldg(&p.bt.tab[(size_t)bn * V + w]);
-            } else {
-                const int2 r = btroot[w];
-                e = make_int2(r.x, __float_as_int(__fsub_rn(__int_as_float(r.y), bU_k)));
-            }
-        }
-        if (lm_on) {
-            float lp;
-            const uint32_t sg = (sbit < 32 ? sglo_k : sghi_k) >> (sbit & 31);
-            const int an = adeg_k & 255, d0 = (adeg_k >> 8) & 255, d1 = (adeg_k >> 16) & 255;
-            const bool arcs_cached = NHW > 0 && aent_k >= 0 && an <= 2 && (an < 1 || d0 <= kACap) && (an < 2 || d1 <= kACap);
-            auto dense = [&](int& nx) -> float {  // the level-1 row / root level
-                if (lmu_k < 0) {
-                    nx = __ldg(&p.lm.uni_next[w]);
-                    return __fadd_rn(cumr_k, __ldg(&p.lm.uni_lp[w]));
-                }
-                int2 de;
-                if (lrow_k >= 0) {
-                    mbar_wait(&rbar[lrow_k], (rp >> lrow_k) & 1u);
-                    de = rows[(size_t)lrow_k * V + w];
-                } else {
-                    de = __ldg(&p.lm.dense[(size_t)lmu_k * V + w]);
-                }
-                nx = de.y & 0x7fffffff;
-                return __fadd_rn((de.y & 0x80000000) ? cumu_k : cumr_k, __int_as_float(de.x));
-            };
-            if (!(sg & 1u) && lrow_k >= 0) {
-                // no arc level holds w: the cached dense row decides
-                lp = dense(ln);
-                ++st_lmr;
-            } else if ((sg & 1u) && arcs_cached) {
-                mbar_wait(&abar[aent_k], (uint32_t)(ap >> aent_k) & 1u);
-                bool hit = false;
-                lp = 0.0f;
-                for (int j = 0; j < an && !hit; ++j) {  // the first (longest-context) level holding w wins
-                    const int4* A = acache + (size_t)(aent_k * 2 + j) * kACap;
-                    int lo = 0, hi = j ? d1 : d0;
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        const int4 a = A[mid];
-                        if (a.x == w) { hit = true; lp = __fadd_rn(j ? acum1_k : acum0_k, __int_as_float(a.y)); ln = a.z; break; }
-                        if (a.x < w) lo = mid + 1; else hi = mid;
-                    }
-                }
-                if (!hit) lp = dense(ln);
-                ++st_lmc;
-            } else {
-                lp = lm_query<LMV>(p.lm, (const int*)(p.lm.rec + (size_t)ln * RW4), w, ln);
-                ++st_lmg;
-            }
-            sx = __fmaf_rn(p.alpha_lm, lp, sx);
-        }
-        if (bt_on) { bn = e.x; sx = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), sx); }
-        return (sx > kNeg && sx >= th) ? make_key(sx, flat_idx(k, w)) : 0ull;
-    };
-
-    // ---- the pair job (helper mode, NHW > 0). Posted by the beam warp after it staged the slot
-    // table (s_acc .. s_rsort: live slots by reach acc + ub, descending); run by all NT threads
-    // between job barriers:
-    //  P1  one pass over the frame row: each token with D[w] >= jb.dt (the listed ones; the
-    //      unlisted ones too when the filter reaches below the record's floor, jb.scan) walks the
-    //      live slots in reach order and gathers the pairs whose bound reaches jb.thr (the bounds
-    //      of the single-warp path, so exactly the same candidates pass);
-    //  P2  one thread per pair scores it exactly (Eq. (1), R19 order); keys >= jb.thr are appended
-    //      to the candidate buffer (anything below cannot enter the TopK or is pruned);
-    //  P3  the rank of every candidate whose score is >= fl(max - θ) (the others are pruned,
-    //      P:138-139, whatever their rank; keys are unique, ties impossible, R9): s_sel[r], r < K.
-    // More than kJobPairs pairs (flat frames, θ = ∞): P2 / P3 are skipped and the beam warp takes
-    // the single-warp path for this frame.
-    unsigned long long st_jeval = 0;
-    auto wappend = [&](bool take, int* counter) -> int {  // warp-aggregated slot in a shared list
-        const unsigned bal = __ballot_sync(0xffffffffu, take);
-        int base = 0;
-        if (bal) {
-            const int leader = __ffs(bal) - 1;
-            if (lane == leader) base = atomicAdd(counter, __popc(bal));
-            base = __shfl_sync(0xffffffffu, base, leader);
-        }
-        return base + __popc(bal & ((1u << lane) - 1u));
-    };
-    auto run_job = [&]() {
-        const int tid = threadIdx.x;
-        const float thj = jb.thr, dt = jb.dt, uam = jb.uamax;
-        const int na = jb.nalive;
-        // P1: one pass over the frame's row (every non-blank token: the listed ones and, when the
-        // filter reaches below the record's floor, the unlisted ones). A token with D >= dt walks
-        // the live slots in reach order until no later slot can reach thj; each pair whose bound
-        // reaches thj is appended. Token wA was scored from every slot by the beam warp already.
-        {
-            const unsigned char* rowb = jb.rowb;
-            const float xt = jb.xthr;
-            const double lse = jb.lse;
-            const bool scan = jb.scan != 0;
-            const int wA = jb.wA;
-            for (int w = tid; w < blank; w += NT) {
-                const float x = BF16 ? bf16f(((const uint16_t*)rowb)[w]) : ((const float*)rowb)[w];
-                if (!(scan || x >= xt) || w == wA) continue;  // unlisted tokens only when scanning
-                const float d = BF16 ? (float)((double)x - lse) : x;
-                if (!(d >= dt)) continue;
-                for (int kk = 0; kk < na; ++kk) {
-                    const float4 sp = s_pack[kk];  // {acc, ub, ua, last << 8 | slot}, by reach desc
-                    const float sfk = __fadd_rn(sp.x, sp.y);
-                    if (__fadd_rn(d, sfk) + 1e-4f * (1.0f + fabsf(d) + fabsf(sfk) + uam) < thj) break;
-                    const int lk = __float_as_int(sp.w);
-                    if (w == (lk >> 8)) continue;  // repeat: scored with the blank candidates
-                    const float s0 = __fadd_rn(sp.x, d);
-                    if (__fadd_rn(s0, sp.y) + 1e-5f * (1.0f + fabsf(s0) + sp.z) >= thj) {
-                        const int e = atomicAdd(&jb.np, 1);
-                        if (e < kJobPairs) jpairs[e] = make_uint2(((uint32_t)(lk & 255) << 16) | (uint32_t)w, __float_as_uint(d));
-                    }
-                }
-            }
-        }
-        job_bar(NT);
-#ifdef FLEXCTC_PHASE_TIMERS
-        if (threadIdx.x == 0) { const long long _n = clock64(); tm[8] += _n - tq; tq = _n; }
-#endif
-        const int np = jb.np;
-        if (np > 0 && np <= kJobPairs) {  // P2
-            const uint32_t rp = jb.rph;
-            uint32_t mx = 0;  // best survivor score (ord_of image)
-            for (int q0 = 0; q0 < np; q0 += NT) {
-                const int q = q0 + tid;
-                uint64_t key = 0;
-                int ln = 0, bn = 0;
-                if (q < np) {
-                    const uint2 pq = jpairs[q];
-                    const int k = (int)(pq.x >> 16), w = (int)(pq.x & 0xffffu);
-                    key = eval(s_acc[k], __uint_as_float(pq.y), w, s_lms[k], s_bts[k], s_row[k], s_cumu[k],
-                               s_cumr[k], s_sglo[k], s_sghi[k], s_bU[k], s_bsglo[k], s_bsghi[k], s_lmu[k], s_aent[k],
-                               s_adeg[k], s_acum0[k], s_acum1[k], k, ln, bn, thj, rp, jb.aph);
-                    ++st_jeval;
-                }
-                const int e = wappend(key != 0ull, &jb.nc);
-                if (key) {
-                    ckey[e] = key; cln[e] = ln; cbn[e] = bn;
-                    mx = max(mx, (uint32_t)(key >> 32));
-                    if (lm_on) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.lm.rec + (size_t)ln * RW4));
-                }
-            }
-            mx = __reduce_max_sync(0xffffffffu, mx);
-            if (lane == 0 && mx) atomicMax(&jb.kmax, mx);
-            job_bar(NT);
-        }
-#ifdef FLEXCTC_PHASE_TIMERS
-        if (threadIdx.x == 0) { const long long _n = clock64(); tm[9] += _n - tq; tq = _n; }
-#endif
-        if (np <= kJobPairs) {  // P3
-            const int n = jb.nc;
-            const uint32_t km = jb.kmax;
-            const uint32_t lo = km ? ord_of(__fsub_rn(ord_inv(km), p.theta)) : 0u;  // keys below: pruned
-            for (int e = tid; e < n; e += NT) {
-                const uint64_t me = ckey[e];
-                if ((uint32_t)(me >> 32) < lo) continue;
-                int r = 0;
-#pragma unroll 4
-                for (int j = 0; j < n; ++j) r += ckey[j] > me ? 1 : 0;
-                if (r < K) s_sel[r] = e;
-            }
-        }
-        job_bar(NT);
-#ifdef FLEXCTC_PHASE_TIMERS
-        if (threadIdx.x == 0) { const long long _n = clock64(); tm[10] += _n - tq; tq = _n; }
-#endif
-    };
-    if (NHW > 0 && threadIdx.x >= 32) {  // helper warps: run the beam warp's pair jobs
-        for (;;) {
-            job_bar(NT);
-            if (jb.cmd == 2) break;
-            run_job();
-        }
-        if (st_jeval) atomicAdd(&p.stats[kEvalSparse], st_jeval);
-        if (st_lmg) atomicAdd(&p.stats[26], st_lmg);
-        if (st_lmr) atomicAdd(&p.stats[27], st_lmr);
-        if (st_lmc) atomicAdd(&p.stats[21], st_lmc);
-        return;
-    }
+    unsigned long long st_batch = 0, st_lmg = 0, st_lmr = 0, st_rowld = 0;
 
     for (;;) {
         int u = 0;
@@ -443,19 +194,10 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
         int arcn = 0, arco0 = 0, arcd0 = 0, arco1 = 0, arcd1 = 0;  // arc levels of the state
         float cumu = 0.0f, cumr = 0.0f, ublm = 0.0f;
         uint32_t sglo = 0, sghi = 0;
-        int aent = -1, adeg = 0;  // helper mode: arc-cache entry of the slot's LM state, its levels
-        float acum0 = 0.0f, acum1 = 0.0f;
         if (lm_on) {
             const int4 h0 = __ldg(p.lm.rec + (size_t)lms * RW4), h1 = __ldg(p.lm.rec + (size_t)lms * RW4 + 1);
             lmu = h0.y; cumu = __int_as_float(h0.z); cumr = __int_as_float(h0.w);
             ublm = __int_as_float(h1.x); sglo = (uint32_t)h1.z; sghi = (uint32_t)h1.w;
-            if (RW4 >= 4) {
-                const int4 h2 = __ldg(p.lm.rec + (size_t)lms * RW4 + 2), h3 = __ldg(p.lm.rec + (size_t)lms * RW4 + 3);
-                arcn = h0.x; arco0 = h2.x; arcd0 = h2.y; arco1 = h2.w; arcd1 = h3.x;
-                acum0 = __int_as_float(h2.z); acum1 = __int_as_float(h3.y);
-                adeg = min(arcn, 255) | (min(arcd0, 255) << 8) | (min(arcd1, 255) << 16);
-            }
-            if (NHW > 0 && lane == 0) { aent = 0; fresh = true; }  // slot 0's <s> state: cache its row and arcs
         }
         float bmaxd = bt_on ? __ldg(&p.bt.maxd[0]) : 0.0f, bU = bt_on ? __ldg(&p.bt.U[0]) : 0.0f;
         uint32_t bsglo = 0, bsghi = 0;  // exception signature of the slot's boost node (root: none)
@@ -467,8 +209,8 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
         for (int t = 0; t < L; ++t) {
             {
                 const int r = t + kWRing - 1;
+                __syncwarp();  // every lane's reads of the previous frame's buffers precede their reuse
                 if (r < L) {
-                    __syncwarp();  // every lane's reads of the slot (frame t - 1) precede its reuse
                     issue(r);
                     nissued = r + 1;
                 }
@@ -582,9 +324,9 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                             if (best == 0xffffffffu) break;  // every row serves a live slot: global path
                             const int v = (int)(best & 31u);
                             if (lane == 0) {
+                                mbar_wait(&rbar[v], (rph >> v) & 1u);  // the row's previous load has landed
                                 rtag[v] = uu;
                                 ruse[v] = t;
-                                rload[v] = t;
                                 fence_proxy_async();
                                 mbar_arrive_tx(&rbar[v], (uint32_t)(V * 8));
                                 bulk_g2s((void*)(rows + (size_t)v * V), p.lm.dense + (size_t)uu * V, (uint32_t)(V * 8), &rbar[v]);
@@ -595,32 +337,13 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                             __syncwarp();
                         }
                     }
+                    __syncwarp();  // the reads of ruse / rtag above precede the next call's writes
             };
             // slots whose state changed at t - 1: get their dense rows now (TMA, lands while the
             // frame runs) and pull the arc lines of their LM state into L1 (the global lookups of
             // later frames then hit L1)
             if (__ballot_sync(0xffffffffu, fresh && alive)) {
                 if (nrow > 0) acquire_rows(fresh);
-                if constexpr (NHW > 0) {
-                    // the new states' arc levels into their arc-cache entries (TMA; levels of more
-                    // than kACap arcs stay global)
-                    const int an = adeg & 255;
-                    const uint32_t b0 = an >= 1 && arcd0 <= kACap ? 16u * (uint32_t)arcd0 : 0u;
-                    const uint32_t b1 = an >= 2 && arcd1 <= kACap ? 16u * (uint32_t)arcd1 : 0u;
-                    const bool go = fresh && alive && lm_on && aent >= 0 && an <= 2 && b0 + b1 > 0 &&
-                                    (an < 1 || arcd0 <= kACap) && (an < 2 || arcd1 <= kACap);
-                    if (go) {
-                        mbar_wait(&abar[aent], (uint32_t)(aph >> aent) & 1u);  // the entry's previous load
-                        fence_proxy_async();
-                        mbar_arrive_tx(&abar[aent], b0 + b1);
-                        if (b0) bulk_g2s(acache + (size_t)aent * 2 * kACap, p.lm.arcs + arco0, b0, &abar[aent]);
-                        if (b1) bulk_g2s(acache + ((size_t)aent * 2 + 1) * kACap, p.lm.arcs + arco1, b1, &abar[aent]);
-                    }
-                    const unsigned long long gm = go ? (1ull << aent) : 0ull;
-                    aph ^= ((unsigned long long)__reduce_or_sync(0xffffffffu, (uint32_t)(gm >> 32)) << 32) |
-                           __reduce_or_sync(0xffffffffu, (uint32_t)gm);
-                    if (fresh && alive && !go) aent = -1;  // not cached: the global search
-                }
                 if (fresh && alive && lm_on) {
                     const int na = min(arcn, 2);
                     for (int j = 0; j < na; ++j) {
@@ -648,6 +371,49 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
             };
             bool scanned = false, paired = false;
             int ntok = 0;
+            // exact score of token w (log-prob d) from a slot given by its fields; key 0 if < thr
+            // boost: from a non-root node u, a token outside u's exception signature has δ(u, w) =
+            // δ(root, w) and delta = fl(delta(root, w) - U(u)) exactly (boost_build.cpp): the root
+            // row in shared memory serves it; signature hits read the transition table
+            auto eval = [&](float acc_k, float d, int w, int lms_k, int bts_k, int lrow_k, float cumu_k, float cumr_k,
+                            uint32_t sglo_k, uint32_t sghi_k, float bU_k, uint32_t bsglo_k, uint32_t bsghi_k, int k,
+                            int& ln, int& bn) -> uint64_t {
+                float sx = __fadd_rn(__fadd_rn(acc_k, d), p.beta);
+                ln = lms_k;
+                bn = bts_k;
+                int2 e = make_int2(0, 0);
+                if (bt_on) {
+                    const int bbit = lm_sig_bit(w);
+                    if (bn == 0) {
+                        e = btroot[w];
+                    } else if (((bbit < 32 ? bsglo_k : bsghi_k) >> (bbit & 31)) & 1u) {
+                        e = __ldg(&p.bt.tab[(size_t)bn * V + w]);
+                    } else {
+                        const int2 r = btroot[w];
+                        e = make_int2(r.x, __float_as_int(__fsub_rn(__int_as_float(r.y), bU_k)));
+                    }
+                }
+                if (lm_on) {
+                    float lp;
+                    const int sbit = lm_sig_bit(w);
+                    const uint32_t sg = (sbit < 32 ? sglo_k : sghi_k) >> (sbit & 31);
+                    if (lrow_k >= 0 && !(sg & 1u)) {
+                        // no arc level holds w: the cached dense row decides (lm_query's dense
+                        // path, the same fp32 operation)
+                        mbar_wait(&rbar[lrow_k], (rph >> lrow_k) & 1u);
+                        const int2 de = rows[(size_t)lrow_k * V + w];
+                        lp = __fadd_rn((de.y & 0x80000000) ? cumu_k : cumr_k, __int_as_float(de.x));
+                        ln = de.y & 0x7fffffff;
+                        ++st_lmr;
+                    } else {
+                        lp = lm_query<LMV>(p.lm, (const int*)(p.lm.rec + (size_t)ln * RW4), w, ln);
+                        ++st_lmg;
+                    }
+                    sx = __fmaf_rn(p.alpha_lm, lp, sx);
+                }
+                if (bt_on) { bn = e.x; sx = __fmaf_rn(p.alpha_bt, __int_as_float(e.y), sx); }
+                return (sx > kNeg && sx >= thr) ? make_key(sx, flat_idx(k, w)) : 0ull;
+            };
             // append the non-zero keys of the lanes, then re-rank and raise thr
             auto push = [&](uint64_t key, int ln, int bn) {
                 ++st_batch;
@@ -700,8 +466,7 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                             if (!rows_ready) { acquire_rows(alive); rows_ready = true; }
                             st_eval += __popc(pb);
                             int ln = 0, bn = 0;
-                            const uint64_t key = pass ? eval(acc, d, w, lms, bts, lrow, cumu, cumr, sglo, sghi, bU, bsglo, bsghi, lmu, aent, adeg, acum0,
-                                                                acum1, lane, ln, bn, thr, rph, aph) : 0ull;
+                            const uint64_t key = pass ? eval(acc, d, w, lms, bts, lrow, cumu, cumr, sglo, sghi, bU, bsglo, bsghi, lane, ln, bn) : 0ull;
                             push(key, ln, bn);
                         }
                     }
@@ -714,7 +479,8 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                 // cheap ones (cached dense row, boost at the root) 32 per round, then the ones that
                 // need the global arc search / boost table together, then one re-rank.
                 bool staged = false;
-                auto stage_slots = [&]() {  // per-slot values for the token lanes; live slots by reach (desc)
+                auto process_B = [&](bool scan, int j_begin, int m) {
+                    if (!staged) {  // per-slot values for the token lanes; live slots by reach (desc)
                         if (!rows_ready) { acquire_rows(alive); rows_ready = true; }
                         const float myr = alive ? __fadd_rn(acc, ub) : kNeg;
                         if (lane < K) {
@@ -723,8 +489,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                             s_row[lane] = lrow; s_cumu[lane] = cumu; s_cumr[lane] = cumr;
                             s_sglo[lane] = sglo; s_sghi[lane] = sghi; s_rs[lane] = myr;
                             s_bU[lane] = bU; s_bsglo[lane] = bsglo; s_bsghi[lane] = bsghi;
-                            s_lmu[lane] = lmu; s_aent[lane] = aent; s_adeg[lane] = adeg;
-                            s_acum0[lane] = acum0; s_acum1[lane] = acum1;
                         }
                         __syncwarp();
                         if (alive) {
@@ -736,14 +500,11 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                             }
                             s_ord[r] = lane;
                             s_rsort[r] = myr;
-                            if (NHW) s_pack[r] = make_float4(acc, ub, ua, __int_as_float((last << 8) | lane));
                         }
                         __syncwarp();
                         staged = true;
                         TQ(1);
-                };
-                auto process_B = [&](bool scan, int j_begin, int m) {
-                    if (!staged) stage_slots();
+                    }
                     for (int j0 = j_begin; j0 < m; j0 += 32) {
                         const int j = j0 + lane;
                         const int w = j < m ? (scan ? (int)tlist[j] : (int)ltok[j]) : -1;
@@ -779,9 +540,7 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                                                 (!bt_on || s_bts[k] == 0 || !(bsg & 1u));
                                         if (cheap)
                                             keyc = eval(s_acc[k], d, w, s_lms[k], s_bts[k], s_row[k], s_cumu[k], s_cumr[k],
-                                                        s_sglo[k], s_sghi[k], s_bU[k], s_bsglo[k], s_bsghi[k], s_lmu[k],
-                                                        s_aent[k], s_adeg[k], s_acum0[k], s_acum1[k], k, lnc, bnc, thr,
-                                                        rph, aph);
+                                                        s_sglo[k], s_sghi[k], s_bU[k], s_bsglo[k], s_bsghi[k], k, lnc, bnc);
                                     }
                                 }
                                 const unsigned pc = __ballot_sync(0xffffffffu, pass && cheap);
@@ -813,13 +572,12 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                                         const int wq = scan ? (int)tlist[j0 + jl] : (int)ltok[j0 + jl];
                                         const float dq = scan ? Dv(wq) : lval[j0 + jl];
                                         key = eval(s_acc[kq], dq, wq, s_lms[kq], s_bts[kq], s_row[kq], s_cumu[kq], s_cumr[kq],
-                                                   s_sglo[kq], s_sghi[kq], s_bU[kq], s_bsglo[kq], s_bsghi[kq], s_lmu[kq],
-                                                   s_aent[kq], s_adeg[kq], s_acum0[kq], s_acum1[kq], kq, ln, bn, thr,
-                                                   rph, aph);
+                                                   s_sglo[kq], s_sghi[kq], s_bU[kq], s_bsglo[kq], s_bsghi[kq], kq, ln, bn);
                                     }
                                     push(key, ln, bn);
                                 }
                             }
+                            __syncwarp();  // the batch's reads of s_pairs precede the next gather
                             TQ(4);
                             if (stop || kk >= nalive) break;
                         }
@@ -828,57 +586,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                 };
                 const float dt0 = dthr_of(thr);
                 const int m0 = __popc(__ballot_sync(0xffffffffu, lane < nlist && lval[lane < nlist ? lane : 0] >= dt0));
-                bool by_job = false;
-                if constexpr (NHW > 0) {
-                    // helper mode: the listed tokens and (below the record's floor) the row scan as
-                    // one pair job of the whole CTA
-                    const bool need_scan = floor_ >= dt0;
-                    // exact pre-check (lane = slot): the pair bound is monotone in D, so if neither the
-                    // slot's best non-repeat listed token in [jA, m0) nor an unlisted token at the
-                    // record's floor (every unlisted D is <= floor) passes, no pair of the slot does
-                    bool cand = false;
-                    if (alive && (m0 > jA || need_scan)) {
-                        int j = jA;
-                        if (j < m0 && (int)ltok[j] == last) ++j;
-                        auto passes = [&](float d) {
-                            const float s0 = __fadd_rn(acc, d);
-                            return __fadd_rn(s0, ub) + 1e-5f * (1.0f + fabsf(s0) + ua) >= thr;
-                        };
-                        if (j < m0) cand = passes(lval[j]);
-                        if (!cand && need_scan) cand = passes(floor_);
-                    }
-                    if (!__any_sync(0xffffffffu, cand)) {
-                        by_job = true;  // nothing can pass: the frame's candidates are complete
-                    } else {
-                        const int best_e = nc > 0 ? s_sel[0] : -1;  // the last rank pass's best entry
-                        stage_slots();
-                        if (lane < K) s_sel[lane] = -1;
-                        if (lane == 0) {
-                            jb.cmd = 1; jb.thr = thr; jb.dt = dt0; jb.uamax = uamax;
-                            jb.jA = jA; jb.m0 = m0; jb.scan = need_scan ? 1 : 0; jb.nalive = nalive;
-                            jb.np = 0; jb.nc = nc; jb.wA = jA ? (int)ltok[0] : -1; jb.t = t; jb.rph = rph; jb.aph = aph; jb.xthr = xthr; jb.rc = rc;
-                            jb.rowb = rowb; jb.lse = lse;
-                            jb.kmax = best_e >= 0 ? (uint32_t)(ckey[best_e] >> 32) : 0u;
-                        }
-                        __syncwarp();
-                        job_bar(NT);
-                        run_job();
-                        if (jb.np <= kJobPairs) {  // else: too many pairs, the single-warp path below
-                            by_job = true;
-                            if (jb.np) paired = true;
-                            nc = jb.nc;
-                            scanned = need_scan;
-                            ntok += m0 - jA;
-                            st_jobs += 1;
-                            st_jpairs += jb.np;
-                            st_jcands += jb.nc;
-                        } else {
-                            rank_pass(nc);  // s_sel was cleared for the job: restore the ranks
-                            st_jover += 1;
-                        }
-                    }
-                }
-                if (!by_job) {
                 if (m0 > jA) { ntok += m0 - jA; process_B(false, jA, m0); }
                 const float dt1 = dthr_of(thr);
 #ifdef FLEXCTC_PHASE_TIMERS
@@ -904,7 +611,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                     ntok += m1;
                     if (m1) process_B(true, 0, m1);
                 }
-                }  // !by_job
             }
             st_frames += 1;
             st_alive += nalive;
@@ -946,10 +652,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
             float n_ublm = 0.0f, n_maxd = 0.0f, n_U = 0.0f, n_cumu = 0.0f, n_cumr = 0.0f;
             uint32_t n_bsglo = 0, n_bsghi = 0;
             int n_lmu = -1, n_lrow = -1, n_arcn = 0, n_arco0 = 0, n_arcd0 = 0, n_arco1 = 0, n_arcd1 = 0;
-            int n_aent = -1, n_adeg = 0;
-            float n_acum0 = 0.0f, n_acum1 = 0.0f;
-            const int p_aent = NHW ? shi(aent, par) : -1, p_adeg = NHW ? shi(adeg, par) : 0;
-            const float p_acum0 = NHW ? shf(acum0, par) : 0.0f, p_acum1 = NHW ? shf(acum1, par) : 0.0f;
             uint32_t n_sglo = 0, n_sghi = 0;
             if (live) {
                 n_acc = s_new;
@@ -966,8 +668,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                         if (RW4 >= 4) {  // arc levels 0 and 1 (same 64-B record line)
                             const int4 h2 = __ldg(p.lm.rec + (size_t)n_lms * RW4 + 2), h3 = __ldg(p.lm.rec + (size_t)n_lms * RW4 + 3);
                             n_arcn = h0.x; n_arco0 = h2.x; n_arcd0 = h2.y; n_arco1 = h2.w; n_arcd1 = h3.x;
-                            n_acum0 = __int_as_float(h2.z); n_acum1 = __int_as_float(h3.y);
-                            n_adeg = min(n_arcn, 255) | (min(n_arcd0, 255) << 8) | (min(n_arcd1, 255) << 16);
                         }
                     }
                     n_maxd = bt_on ? __ldg(&p.bt.maxd[n_bts]) : 0.0f;
@@ -979,7 +679,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
                 } else {
                     n_ublm = p_ublm; n_maxd = p_maxd; n_U = p_U; n_bsglo = p_bsglo; n_bsghi = p_bsghi;
                     n_lmu = p_lmu; n_lrow = p_lrow; n_cumu = p_cumu; n_cumr = p_cumr; n_sglo = p_sglo; n_sghi = p_sghi;
-                    n_aent = p_aent; n_adeg = p_adeg; n_acum0 = p_acum0; n_acum1 = p_acum1;
                 }
                 const int64_t o = bp_base + (int64_t)t * K + lane;
                 p.bp_parent[o] = (uint8_t)par;
@@ -987,27 +686,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
             }
             if (lane < K && ((t % kChunk) == kChunk - 1 || t == L - 1))
                 p.chunk_anc[((int64_t)b * p.nch + t / kChunk) * K + lane] = (uint8_t)n_anc;
-            if constexpr (NHW > 0) {
-                // arc-cache entries: a carried state keeps its parent's entry; each emitted state takes
-                // a free one (2K entries, at most K kept: enough for every emission)
-                if (lm_on) {
-                    const bool keep = live && !emit && n_aent >= 0;
-                    const unsigned long long km = keep ? (1ull << n_aent) : 0ull;
-                    const uint32_t klo = __reduce_or_sync(0xffffffffu, (uint32_t)km);
-                    const uint32_t khi = __reduce_or_sync(0xffffffffu, (uint32_t)(km >> 32));
-                    const bool need = live && emit;
-                    const unsigned emb = __ballot_sync(0xffffffffu, need);
-                    if (need) {
-                        const int rk = __popc(emb & ((1u << lane) - 1u));
-                        const uint32_t flo = ~klo & (nae >= 32 ? 0xffffffffu : ((1u << nae) - 1u));
-                        const uint32_t fhi = nae > 32 ? ~khi & (nae >= 64 ? 0xffffffffu : ((1u << (nae - 32)) - 1u)) : 0u;
-                        const int nlo = __popc(flo);
-                        n_aent = rk < nlo ? (int)__fns(flo, 0, rk + 1) : 32 + (int)__fns(fhi, 0, rk - nlo + 1);
-                    } else if (!keep) {
-                        n_aent = -1;
-                    }
-                }
-            }
 
             [[maybe_unused]] const long long c_e = WCLK();
             // ------------------------------------------------ RecombineHypotheses
@@ -1040,16 +718,15 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
             anc = n_anc;
             ublm = n_ublm;
             bmaxd = n_maxd;
-            bU = n_U;
             bsglo = n_bsglo; bsghi = n_bsghi;
+            bU = n_U;
             lmu = n_lmu; lrow = n_lrow; cumu = n_cumu; cumr = n_cumr; sglo = n_sglo; sghi = n_sghi;
             fresh = emit;
             arcn = n_arcn; arco0 = n_arco0; arcd0 = n_arcd0; arco1 = n_arco1; arcd1 = n_arcd1;
-            aent = n_aent; adeg = n_adeg; acum0 = n_acum0; acum1 = n_acum1;
             if (!(acc > kNeg)) {
                 acc = kNeg; last = blank; hash = 0ull; lms = 0; bts = 0; ublm = 0.0f; bmaxd = 0.0f; bU = 0.0f;
                 bsglo = 0; bsghi = 0;
-                lmu = -1; lrow = -1; aent = -1;
+                lmu = -1; lrow = -1;
             }
 #ifdef FLEXCTC_PHASE_TIMERS
             {
@@ -1180,12 +857,6 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
         }
         __syncwarp();
     }
-    if constexpr (NHW > 0) {  // release the helper warps
-        if (lane == 0) jb.cmd = 2;
-        __syncwarp();
-        job_bar(NT);
-        if (st_jeval) atomicAdd(&p.stats[kEvalSparse], st_jeval);
-    }
     if (lane == 0) {
         atomicAdd(&p.stats[kFrames], st_frames);
         atomicAdd(&p.stats[kAlive], st_alive);
@@ -1195,18 +866,11 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
         atomicAdd(&p.stats[kHeavyFrames], st_pairfr);   // frames with candidate pairs
         atomicAdd(&p.stats[24], st_batch);   // scoring batches (one ballot of pairs)
         atomicAdd(&p.stats[25], st_rowld);   // dense rows loaded into the cache
-        if (NHW) {
-            atomicAdd(&p.stats[28], st_jobs);     // pair jobs (helper mode)
-            atomicAdd(&p.stats[29], st_jpairs);   // pairs they scored
-            atomicAdd(&p.stats[23], st_jcands);   // candidates they ranked
-            atomicAdd(&p.stats[22], st_jover);    // jobs too large (single-warp path)
-        }
     }
     {  // per-lane counts: LM lookups through the global arc search / the cached dense rows
         const unsigned long long a = st_lmg, c = st_lmr;
         atomicAdd(&p.stats[26], a);
         atomicAdd(&p.stats[27], c);
-        if (NHW && st_lmc) atomicAdd(&p.stats[21], st_lmc);  // LM lookups served by the arc cache
     }
     if (lane == 0) {
 #ifdef FLEXCTC_PHASE_TIMERS
@@ -1218,57 +882,17 @@ __global__ void __launch_bounds__(32 * (NHW ? NHW + 1 : kWBMax)) warp_beam_kerne
 }  // namespace
 
 // Warp-per-utterance beam path (K <= 32): frame_compact_kernel (launched by the caller) then
-// this kernel. Helper mode (FLEXCTC_HELPERS=1, the batch fits the GPU at one utterance per SM, a
-// <= 4-gram LM or none): one utterance per CTA, a beam warp plus kHelpers helper warps for the
-// pair jobs. Otherwise warps per CTA: 1 while the batch fits the SMs, else up to kWBMax, as
-// shared memory allows.
-constexpr int kHelpers = 7;
-
+// this kernel. Warps per CTA: 1 while the batch fits the SMs (one utterance per SM: the
+// shortest frame step), else up to kWBMax, as shared memory allows.
 size_t warp_beam_smem_per_warp(int Vp1, bool bf16, int nch) { return wlayout(Vp1, bf16 ? 2 : 4, nch, 0).total; }
-
-bool warp_helper_mode(const DecodeParams& p, int nsm) {
-    const bool small_lm = !p.use_lm || p.lm.NL <= 2;
-    if (!small_lm) return false;
-    // opt-in (measured slower than the persistent CTA kernel at c4: 1.98-2.4 vs 1.59 ms per
-    // decode, profiles/r2/helper_mode_c4.jsonl); FLEXCTC_HELPERS=1 selects it for B <= #SMs
-    const char* e = getenv("FLEXCTC_HELPERS");
-    return e && e[0] == '1' && p.B <= nsm;
-}
 
 int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev0, void* ev1, std::string& err) {
     cudaStream_t st = (cudaStream_t)stream;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int esz = bf16 ? 2 : 4;
+    const size_t per = wlayout(p.Vp1, bf16 ? 2 : 4, p.nch, 0).total;
     const size_t root = p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0;
-    const char* e_rows = getenv("FLEXCTC_WARP_ROWS");  // A/B switch: cap of the dense-row cache
-    if (warp_helper_mode(p, nsm)) {
-        const size_t job = 8 * (size_t)kJobPairs;
-        const size_t per = wlayout(p.Vp1, esz, p.nch, 0, kHelpCandCap, 2 * p.K).total;
-        if (per + root + job > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
-        int nrow = 0;
-        if (p.use_lm && ((p.Vp1 - 1) & 1) == 0) {
-            const size_t rowb = (size_t)(p.Vp1 - 1) * 8 + 16;
-            nrow = (int)std::min<size_t>(16, (200 * 1024 - (per + root + job)) / rowb);
-            if (e_rows) nrow = std::min(nrow, std::max(0, atoi(e_rows)));
-        }
-        const size_t smem = wlayout(p.Vp1, esz, p.nch, nrow, kHelpCandCap, 2 * p.K).total + root + job;
-        void (*kern)(const DecodeParams, int) = bf16 ? warp_beam_kernel<2, true, kHelpers> : warp_beam_kernel<2, false, kHelpers>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int occ = 0;
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * (kHelpers + 1), smem);
-        if (e != cudaSuccess || occ < 1) { err = e != cudaSuccess ? cudaGetErrorString(e) : "occupancy query failed"; return 1; }
-        const int grid = std::min(p.B, nsm * occ);
-        if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
-        kern<<<grid, 32 * (kHelpers + 1), smem, st>>>(p, nrow);
-        set_kernel_name("warp_beam_kernel+helpers");
-        e = cudaGetLastError();
-        if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
-        if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-        return 0;
-    }
-    const size_t per = wlayout(p.Vp1, esz, p.nch, 0).total;
     int wpc = std::min(kWBMax, std::max(1, (p.B + nsm - 1) / nsm));
     while (wpc > 1 && wpc * per + root > 200 * 1024) --wpc;
     // dense-row cache: as many rows (<= 16) as the shared memory left per warp holds
@@ -1277,15 +901,15 @@ int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev0, 
         const size_t rowb = (size_t)(p.Vp1 - 1) * 8 + 16;
         const size_t left = 200 * 1024 - (wpc * per + root);
         nrow = (int)std::min<size_t>(16, left / (wpc * rowb));
-        if (e_rows) nrow = std::min(nrow, std::max(0, atoi(e_rows)));
+        if (const char* e = getenv("FLEXCTC_WARP_ROWS")) nrow = std::min(nrow, std::max(0, atoi(e)));  // A/B switch
     }
-    const size_t per2 = wlayout(p.Vp1, esz, p.nch, nrow).total;
+    const size_t per2 = wlayout(p.Vp1, bf16 ? 2 : 4, p.nch, nrow).total;
     const size_t smem = wpc * per2 + root;
     if (smem > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
     const bool small_lm = !p.use_lm || p.lm.NL <= 2;
     void (*kern)(const DecodeParams, int);
-    if (small_lm) kern = bf16 ? warp_beam_kernel<2, true, 0> : warp_beam_kernel<2, false, 0>;
-    else kern = bf16 ? warp_beam_kernel<kMaxLmLevels, true, 0> : warp_beam_kernel<kMaxLmLevels, false, 0>;
+    if (small_lm) kern = bf16 ? warp_beam_kernel<2, true> : warp_beam_kernel<2, false>;
+    else kern = bf16 ? warp_beam_kernel<kMaxLmLevels, true> : warp_beam_kernel<kMaxLmLevels, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * wpc, smem);

@@ -5,8 +5,8 @@
 Covers the beam-warp + helpers mode (K <= 32, LM + boosting), the whole-CTA mode (K = 64), the
 single-warp launch, the greedy kernels (plain and fused, K = 1; TMA bulk rows + mbarriers), the
 n-best output, the bf16-logits input pass and the streamed host path, on a few short utterances,
-and checks the results against the oracle. Round 2: the compaction pass, the warp kernel alone and
-in helper mode, and the CTA kernel reading compaction records."""
+and checks the results against the oracle. Round 2: the compaction pass, the warp kernel, and the
+CTA kernel reading compaction records."""
 import os
 import sys
 
@@ -80,10 +80,10 @@ def run_more():
 
 
 def run_round2():
-    """Round 2 kernels: the compaction pass + warp kernel (alone and in helper mode: pair jobs,
-    boost signatures, LM arc cache, TMA rings), the CTA kernel reading compaction records (K = 16
-    beam-warp mode and K = 64 whole-CTA mode)."""
-    for env, K in ((dict(FLEXCTC_WARP="1", FLEXCTC_HELPERS="0"), 16), (dict(FLEXCTC_WARP="1", FLEXCTC_HELPERS="1"), 16),
+    """Round 2 kernels: the compaction pass + warp kernel (TMA rings, dense-row cache with
+    evictions, boost signatures), the CTA kernel reading compaction records (K = 16 beam-warp mode
+    and K = 64 whole-CTA mode)."""
+    for env, K in ((dict(FLEXCTC_WARP="1"), 16), (dict(FLEXCTC_WARP="1", FLEXCTC_WARP_ROWS="2"), 16),
                    (dict(FLEXCTC_WARP="0", FLEXCTC_CMP="1"), 16), (dict(FLEXCTC_CMP="1"), 64)):
         os.environ.update(env)
         try:

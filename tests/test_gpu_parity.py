@@ -290,7 +290,7 @@ def test_empty_batch_and_zero_lengths(lm_pair):
 def test_decode_host_end_to_end(lm_pair, bt_pair, wname, B, streamed, monkeypatch):
     """flexctc_decode_host (H2D in frame chunks overlapping the persistent kernel, or copy-then-
     decode) returns exactly what flexctc_decode returns on the same inputs: fixed lengths (2D
-    chunk copies), ragged LibriSpeech-shaped lengths (batched per-utterance copies), tiny c1."""
+    chunk copies), ragged LibriSpeech-shaped lengths (pinned: the gather kernel), tiny c1."""
     if not streamed:
         monkeypatch.setenv("FLEXCTC_NO_STREAM_INPUT", "1")
     assert F.host_streaming() == streamed  # the B200 image supports stream memory operations
@@ -307,6 +307,19 @@ def test_decode_host_end_to_end(lm_pair, bt_pair, wname, B, streamed, monkeypatc
         assert np.array_equal(out["tokens"].numpy(), g["tokens"])
         assert np.array_equal(out["timestamps"].numpy(), g["timestamps"])
         assert np.array_equal(out["scores"].numpy().view(np.int32), g["scores"].view(np.int32))
+
+
+def test_decode_host_ragged_pageable(lm_pair, bt_pair):
+    """Ragged lengths from a pageable (not device-mapped) host buffer: the streamed path falls back
+    from the gather kernel to 2D copies of runs of live utterances; same outputs as flexctc_decode."""
+    assert F.host_streaming()
+    wl, D, L, _, _ = synth.workload_inputs("c5", B=24)
+    cfg = wl_cfg(wl, beam=16)
+    out = F.decode_host(np.ascontiguousarray(D), L.astype(np.int32), cfg, lm_pair[0], bt_pair[0])
+    g = gpu_decode(D, L, cfg, lm_pair[0], bt_pair[0])
+    assert np.array_equal(out["tokens"].numpy(), g["tokens"])
+    assert np.array_equal(out["timestamps"].numpy(), g["timestamps"])
+    assert np.array_equal(out["scores"].numpy().view(np.int32), g["scores"].view(np.int32))
 
 
 def test_decode_refuses_host_memory_through_abi():

@@ -22,9 +22,8 @@ from tests.test_gpu_parity import gpu_decode, run_pair, wl_cfg  # noqa: E402
 
 
 def _path(monkeypatch, warp):
-    """"0": the persistent CTA kernel, "1": the warp kernel, "h": the warp kernel in helper mode."""
-    monkeypatch.setenv("FLEXCTC_WARP", "0" if warp == "0" else "1")
-    monkeypatch.setenv("FLEXCTC_HELPERS", "1" if warp == "h" else "0")
+    """"0": the persistent CTA kernel, "1": the warp kernel."""
+    monkeypatch.setenv("FLEXCTC_WARP", warp)
 
 
 def _peaky(align, Vp1, p):
@@ -33,7 +32,7 @@ def _peaky(align, Vp1, p):
     return np.log(D)
 
 
-@pytest.mark.parametrize("warp", ["0", "1", "h"])
+@pytest.mark.parametrize("warp", ["0", "1"])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_timestamp_fixtures(golden, monkeypatch, warp, mode):
     _path(monkeypatch, warp)
@@ -47,7 +46,7 @@ def test_timestamp_fixtures(golden, monkeypatch, warp, mode):
         assert out["alignment"][0].tolist() == case["align"]
 
 
-@pytest.mark.parametrize("warp", ["0", "1", "h"])
+@pytest.mark.parametrize("warp", ["0", "1"])
 def test_topk_tie_fixture(golden, monkeypatch, warp):
     _path(monkeypatch, warp)
     g = golden["decode"]["topk_tie"]
@@ -63,7 +62,7 @@ def test_topk_tie_fixture(golden, monkeypatch, warp):
         assert float(nb["scores"][0, 0]) == float(nb["scores"][0, 1])
 
 
-@pytest.mark.parametrize("warp", ["0", "1", "h"])
+@pytest.mark.parametrize("warp", ["0", "1"])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_merge_tie_fixture(golden, monkeypatch, warp, mode):
     _path(monkeypatch, warp)
@@ -93,15 +92,11 @@ def test_c4_shaped_large_batches(lm_pair, bt_pair, B):
     run_pair(D, L, wl_cfg(wl), lm_pair[0], lm_pair[1], bt_pair[0], bt_pair[1], ctx=f"c4 B={B}")
 
 
-@pytest.mark.parametrize("helpers", ["0", "1"])
 @pytest.mark.parametrize("wname", ["c2", "c3", "c4"])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_warp_kernel_forced(lm_pair, bt_pair, monkeypatch, wname, mode, helpers):
-    """The warp kernel (and its compaction pass) at the small-batch configurations, alone and in
-    helper mode (beam warp + 7 helper warps per utterance: pair jobs, boost signature, LM arc
-    cache)."""
+def test_warp_kernel_forced(lm_pair, bt_pair, monkeypatch, wname, mode):
+    """The warp kernel (and its compaction pass) at the small-batch configurations."""
     monkeypatch.setenv("FLEXCTC_WARP", "1")
-    monkeypatch.setenv("FLEXCTC_HELPERS", helpers)
     wl, D, L, _, _ = synth.workload_inputs(wname)
     glm, olm = (lm_pair[0], lm_pair[1]) if wl.lm else (None, None)
     gbt, obt = (bt_pair[0], bt_pair[1]) if wl.boost else (None, None)
@@ -129,12 +124,10 @@ def test_cta_kernel_with_compaction_records_k128(lm_pair, bt_pair, monkeypatch):
     run_pair(D, L, wl_cfg(wl), lm_pair[0], lm_pair[1], bt_pair[0], bt_pair[1], ctx="records c5 B=24")
 
 
-@pytest.mark.parametrize("helpers", ["0", "1"])
 @pytest.mark.parametrize("rows", ["0", "4"])
-def test_warp_kernel_row_cache_sizes(lm_pair, bt_pair, monkeypatch, rows, helpers):
+def test_warp_kernel_row_cache_sizes(lm_pair, bt_pair, monkeypatch, rows):
     """The warp kernel with the dense-row cache off / tiny (evictions on every frame) at c4."""
     monkeypatch.setenv("FLEXCTC_WARP", "1")
-    monkeypatch.setenv("FLEXCTC_HELPERS", helpers)
     monkeypatch.setenv("FLEXCTC_WARP_ROWS", rows)
     wl, D, L, _, _ = synth.workload_inputs("c4", B=16)
     run_pair(D, L, wl_cfg(wl), lm_pair[0], lm_pair[1], bt_pair[0], bt_pair[1], ctx=f"rows {rows}")

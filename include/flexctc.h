@@ -238,11 +238,12 @@ flexctc_status flexctc_set_stage_events(int32_t stage, void* ev_start, void* ev_
 const char* flexctc_last_kernel(void);
 
 /* Device counters of the last decode that used `workspace` (call after the stream has
- * synchronised); copies min(n, 32) u64 values: frames, sum of live slots, sum of listed tokens,
+ * synchronised); copies min(n, 48) u64 values: frames, sum of live slots, sum of listed tokens,
  * sparse exact evaluations, dense frames, LM rows built, dense exact evaluations, buffer
  * compactions, top-token stages, deferred next-state queries, then SM cycles (summed over CTAs,
  * thread 0) of frame phases 1-3, 4, LM row builds, 5, 6-7, the count of frames with listed
- * tokens and their cycles. */
+ * tokens and their cycles, finer phase cycles (timers builds), and at word 35 the frames the CTA
+ * kernel's settled-beam fast path took. The warp kernel reuses words 21-29 for its own counters. */
 flexctc_status flexctc_get_stats(const void* workspace, uint64_t* out, int32_t n);
 
 /* Reads the device flags of the last decode that used `workspace` (call after the stream has

@@ -84,7 +84,7 @@ struct Shared {
 };
 
 struct Scalars {
-    int nbuf, m, nalive, nsel, u, npair, excl, scan;
+    int nbuf, m, nalive, nsel, u, npair, excl, scan, fast;
     float thr, ubvmax, dthr;
     uint64_t kth;
     float rf[4][32];
@@ -316,7 +316,8 @@ __device__ void build_lm_row(const LmDev& lm, int state, float* row, int V) {
 // warps are helpers. A template parameter so the group size of the slot-parallel phases is a
 // compile-time constant.
 // compile-time V', K, LM record width (0 = runtime); FUS (0 = runtime): bit 0 LM, bit 1 boosting,
-// bit 2 "plain" = no LM-row cache (nrow 0), log-sum-exp merges, non-negative fusion weights
+// bit 2 "plain" = no LM-row cache (nrow 0), log-sum-exp merges, non-negative fusion weights; bit 3 =
+// read the compaction records (FLEXCTC_CMP=1)
 template <int NT, int LMV, bool SOLO, int VPC = 0, int KC = 0, int RWC = 0, int FUS = 0>
 __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, const int ring_rows, const int cap,
                                                       int nrow, const int dense_min) {
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     // beam warp only for frames whose candidate list the summary cannot provide.
     constexpr int kListCap = 32;
     constexpr float kListDelta = 16.0f;
-    constexpr int kRing = 4;
+    constexpr int kRing = 4;  // frame rows in flight (cp.async ring; R = kRing for V' <= 2048)
     __shared__ unsigned long long s_sum_key[kRing];
     __shared__ float s_sum_floor[kRing];
     __shared__ int s_sum_cnt[kRing];
@@ -357,10 +358,13 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const int RWS = RWC ? RWC : lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     constexpr bool plain = (FUS & 4) != 0;
     const bool ub_inf = plain ? false : (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
-    const bool use_cmp = FUS ? false : p.use_cmp != 0;  // records (FLEXCTC_CMP=1): generic variants only
+    // compaction records: the generic variants follow p.use_cmp; specialised ones compile them in
+    // (FUS bit 3) or out
+    const bool use_cmp = FUS ? (FUS & 8) != 0 : p.use_cmp != 0;
     const int merge_mode = plain ? 0 : p.merge_mode;
     if (plain) nrow = 0;
     constexpr bool solo = SOLO;  // host: K <= 32 && NT >= 128 && R == kRing && !solo_off (>= 3 helper warps)
+    constexpr int kPfSolo = kRing - 2;  // solo mode: helpers copy row t + 2 while the beam warp reads row t
     const bool helper = solo && tid >= 32;
     const bool bw = !solo || tid < 32;               // takes part in the slot-serial phases
     const int ltid = helper ? tid - 32 : tid;        // row loader index / count
@@ -436,6 +440,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         const int b = p.order[u];
         const int L = p.len_c[b];
         const float* Db = p.log_probs + (int64_t)b * p.stride_b;
+        if (tid == 0) sc.fast = 0;
         ready = 0;  // streamed input: what this thread has seen landed, per utterance
         const int64_t bp_base = (int64_t)b * p.T * K;  // backpointers of this utterance
 
@@ -458,9 +463,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 c0.btm[1] = bt_on ? __ldg(&p.bt.U[0]) : 0.0f;
             }
         }
-        // Row prefetch: in solo mode the helper warps own the ring (distance 2, so the beam warp
-        // can still read row t while helpers fill row t+2); otherwise all threads (distance R-1).
-        const int pf = solo ? 2 : R - 1;
+        // Row prefetch: in solo mode the helper warps own the ring (distance R - 2, so the beam warp
+        // can still read rows t - 1 and t while helpers fill row t + 2); otherwise all threads (distance R - 1).
+        const int pf = solo ? kPfSolo : R - 1;
         if (!solo || helper)
             for (int r = 0; r < pf; ++r) {  // prologue
                 if (r < L) {
@@ -473,8 +478,12 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 cp_commit();
             }
 
+        int cbank = 0;      // current bank (every thread tracks it, helpers included)
+        bool flip = false;  // the previous frame wrote the other bank (a fast-path frame updates in place)
         for (int t = 0; t < L; ++t) {
-            const int cb = t & 1;  // current bank (every thread tracks it, helpers included)
+            if (flip) cbank ^= 1;
+            flip = true;
+            const int cb = cbank;
             const Bank cur = bank(cb);
             const Bank nxt = bank(cb ^ 1);
             const long long ctop = TCLK();
@@ -491,7 +500,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                                    p.cmp + ((int64_t)b * p.T + r) * kCmpBytes + 16 * ltid);
                 }
                 cp_commit();
-                if (solo) cp_wait<2>(); else if (R == 4) cp_wait<3>(); else cp_wait<1>();
+                if (solo) cp_wait<kPfSolo>(); else if (R == 4) cp_wait<3>(); else cp_wait<1>();
             }
             // the compaction pass's record of frame t (use_cmp): D[blank], the listed tokens sorted by
             // (D desc, token asc) and floor >= every unlisted D; n = 0 with floor = +inf: no usable list
@@ -540,6 +549,9 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                         base = __shfl_sync(0xffffffffu, base, 0);
                         const int q = base + __popc(bal & ((1u << (tid & 31)) - 1u));
                         if (hit && q < kListCap) { s_list_tok[slot * kListCap + q] = w; s_list_d[slot * kListCap + q] = row[w]; }
+                        // the list overflowed: the beam warp only tests count > kListCap, so this
+                        // warp's further hits change nothing
+                        if (base + __popc(bal) > kListCap) break;
                     }
                 }
                 if (h == 0) { s_sum_key[slot] = best; s_sum_floor[slot] = floor_; }
@@ -554,7 +566,62 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             long long tp1 = c0, tp2 = c0, tp3 = c0;  // phase boundaries (timers build, thread 0)
             bool stage_a = false;
             int wstar = -1;
-            if (bw) {
+            // Settled-beam fast path (K <= 32, beam warp): every live slot's last label is blank, the
+            // live slots are a prefix in (score desc, slot asc) order after adding D[blank], and no
+            // non-blank token can reach fl(max - θ) (the token filter of phase 3 with thr = τ0). Then
+            // Alg. 1 reduces to acc_k += D[blank] for every slot (no repeat candidates, no emission,
+            // TopK = the slots in their own order, no recombination: the (hash, blank) keys are
+            // distinct) and the θ-prune; the bank is updated in place.
+            bool fast = false;
+            if (solo && bw && !p.fast_off) {
+                const float a = tid < K ? cur.acc[tid] : kNeg;
+                const bool al = a > kNeg;
+                const int lk = tid < K ? cur.last[tid] : blank;
+                const unsigned am = __ballot_sync(0xffffffffu, al);
+                const int na = __popc(am);
+                const float nw = al ? __fadd_rn(a, row[blank]) : kNeg;
+                const float nx = __shfl_down_sync(0xffffffffu, nw, 1);
+                bool ok = (!al || lk == blank) && (tid + 1 >= na || nw >= nx);
+                ok = __all_sync(0xffffffffu, ok) && na > 0 && am == (na == 32 ? 0xffffffffu : (1u << na) - 1u);
+                if (ok) {
+                    float ub = kNeg;
+                    if (al) {
+                        ub = p.beta;
+                        if (lm_on) ub += p.alpha_lm * __int_as_float(recof(cur, tid)[4]);
+                        if (bt_on) ub += p.alpha_bt * cur.btm[2 * tid];
+                        if (ub_inf) ub = INFINITY;
+                    }
+                    const float accmax = score_of((uint64_t)__reduce_max_sync(0xffffffffu, ord_of(al ? a : kNeg)) << 32);
+                    const float ubvmax = score_of((uint64_t)__reduce_max_sync(0xffffffffu, ord_of(ub)) << 32);
+                    const float mx = __shfl_sync(0xffffffffu, nw, 0);
+                    const float tau0 = __fsub_rn(mx, p.theta);
+                    const float dstar = score_of(s_sum_key[slot]);
+                    const float mg = 1e-4f * (1.0f + fabsf(tau0) + fabsf(accmax) + fabsf(ubvmax));
+                    const float dthr = __fsub_rn(__fsub_rn(__fsub_rn(tau0, accmax), ubvmax), mg);
+                    fast = mx > kNeg && !(dstar >= dthr);
+                    if (fast && tid < K) {
+                        const int64_t bpo = bp_base + (int64_t)(t * K);
+                        uint8_t my_anc = 0;
+                        if (al && nw >= tau0) {  // survives the θ-prune: parent = itself, label = blank
+                            cur.acc[tid] = nw;
+                            my_anc = (t % kChunk == 0) ? (uint8_t)tid : cur.anc[tid];
+                            cur.anc[tid] = my_anc;
+                            p.bp_parent[bpo + tid] = (uint8_t)tid;
+                            p.bp_label[bpo + tid] = (uint16_t)blank;
+                        } else if (al) {
+                            cur.acc[tid] = kNeg; cur.last[tid] = blank; cur.hash[tid] = 0ull;
+                            cur.lms[tid] = 0; cur.bts[tid] = 0; cur.anc[tid] = 0;
+                        }
+                        if ((t % kChunk) == kChunk - 1 || t == L - 1)
+                            p.chunk_anc[((int64_t)b * p.nch + t / kChunk) * K + tid] = my_anc;
+                    }
+                }
+                if (tid == 0) {
+                    sc.fast = fast ? 1 : 0;
+                    if (fast) { sc.scan = 0; sc.m = 0; st[kFastFrames] += 1; st[kFrames] += 1; }
+                }
+            }
+            if (bw && !fast) {
                 // ------------------------------------------------ phase 1: exact blank/repeat candidates,
                 // per-slot bounds, frame argmax over non-blank tokens, alive list
                 float a = kNeg, sbk = kNeg, srk = kNeg, ubk = kNeg;
@@ -696,6 +763,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             tp3 = TCLK();
             if (solo) __syncthreads();  // B1: the helpers learn whether this frame needs them
             gsync(G);
+            if (solo && sc.fast) {  // fast-path frame: updated in place, nothing more to do
+                if (tid == 0) st[kCycFast] += (uint32_t)(TCLK() - c0);
+                flip = false;
+                continue;
+            }
             const bool scan_all = sc.scan;
             const int nalive = sc.nalive;
             const float ubvmax = sc.ubvmax;
@@ -1113,7 +1185,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         }
         cp_wait<0>();
         __syncthreads();  // join the beam warp and the helpers (solo mode)
-        const Bank cur = bank(L & 1);
+        const Bank cur = bank(flip ? cbank ^ 1 : cbank);
 
         // ------------------------------------------------------------ EOS + final merge (R15)
         float fs = kNeg;
@@ -1346,6 +1418,9 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
         if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 15>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
+        if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 5>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
         if (e == cudaSuccess)
@@ -1364,6 +1439,8 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
     DecodeParams q = p;
     const char* e_solo = getenv("FLEXCTC_SOLO");  // "0": every phase uses the whole CTA (test switch)
     q.solo_off = (e_solo && e_solo[0] == '0') ? 1 : 0;
+    const char* e_fast = getenv("FLEXCTC_FAST");  // "0": no settled-beam fast path (A/B switch)
+    q.fast_off = (e_fast && e_fast[0] == '0') ? 1 : 0;
     const bool solo = p.K <= 32 && NT >= 128 && pl.R == 4 && !q.solo_off;  // 4 = the kernel's kRing
     if (ev0 && ev1) cudaEventRecord((cudaEvent_t)ev0, st);
     if constexpr (NT >= 128) {
@@ -1374,6 +1451,8 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
                                    p.alpha_bt >= 0.0f;
                 if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // the north-star decode
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                else if (solo && p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // ... reading records
+                    ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 15><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && !p.use_bt && plain)  // LM only (c3)
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 5><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt)  // beam 16, 4-gram LM, boosting

@@ -224,7 +224,9 @@ enum Stat { kFrames, kAlive, kListed, kEvalSparse, kDenseFrames, kRowsBuilt, kEv
             // 5, 6, 7
             kLightFrames, kLP1, kLP2, kLP3, kLB1, kLP5, kLP6, kLP7,
             // phase 7 of those frames: match.any, merge scores, chunk ancestors + records, final sync
-            kLP7a, kLP7b, kLP7c, kLP7d, kNumStats };
+            kLP7a, kLP7b, kLP7c, kLP7d,
+            // frames taken by the CTA kernel's settled-beam fast path
+            kFastFrames, kCycFast, kNumStats };
 
 }  // namespace dev
 }  // namespace flexctc

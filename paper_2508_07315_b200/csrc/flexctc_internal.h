@@ -116,6 +116,7 @@ struct DecodeParams {
     int32_t merge_mode, retract, fuse_rep;
     int32_t use_lm, use_bt;
     int32_t solo_off;     // tuning/test switch: disable the beam-warp + helpers mode
+    int32_t fast_off;     // A/B switch (FLEXCTC_FAST=0): disable the CTA kernel's settled-beam fast path
     // streamed input (flexctc_decode_host): frames [0, *ready) of every utterance have landed in
     // log_probs; the row loaders poll it (ld.acquire) before issuing a row. NULL = all resident.
     const uint32_t* ready;

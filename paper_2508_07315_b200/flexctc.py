@@ -59,7 +59,7 @@ STAT_NAMES = ["frames", "alive_slots", "listed_tokens", "exact_sparse", "dense_f
               "cyc_phase1_3", "cyc_phase4", "cyc_lm_rows", "cyc_phase5", "cyc_phase6_7", "heavy_frames",
               "cyc_heavy_frames", "cyc_frame_top", "cyc_phase2", "cyc_phase3", "cyc_p4_setup", "cyc_p4_collect",
               "cyc_p4_eval", "light_frames", "lcyc_p1", "lcyc_p2", "lcyc_p3", "lcyc_b1", "lcyc_p5", "lcyc_p6",
-              "lcyc_p7", "lcyc_p7a", "lcyc_p7b", "lcyc_p7c", "lcyc_p7d"]
+              "lcyc_p7", "lcyc_p7a", "lcyc_p7b", "lcyc_p7c", "lcyc_p7d", "fast_frames", "cyc_fast"]
 
 
 def _load() -> ctypes.CDLL:

@@ -1611,13 +1611,26 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
         return rc;
     }
     const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
-    // FLEXCTC_CMP=1: the persistent CTA kernel reads the frame records of the compaction pass (the
-    // best token, the listed band and its floor) instead of computing per-frame summaries from the
-    // rows. Opt-in: the pass costs more than it saves at c4 / c5 (profiles/r2/cta_records_ab.jsonl:
-    // c4 1.661 -> 1.672 ms, c5 5.873 -> 5.961 ms per decode)
+    // The persistent CTA kernel reads the frame records of the compaction pass (the best token, the
+    // listed band and its floor) instead of computing per-frame summaries from the rows when the
+    // log-probs are resident and the decode has the north-star shape at B <= #SMs (beam 16,
+    // V' = 1025, 4-gram LM + boosting: its specialised variant reads records, and with the
+    // settled-beam fast path the helper warps' summaries are on the critical path: c4 1.542 ->
+    // 1.535 ms per decode including the pass, profiles/r2/ab_records_fastpath.jsonl). Elsewhere the
+    // pass costs more than it saves (c5 5.873 -> 5.961 ms, profiles/r2/cta_records_ab.jsonl).
+    // FLEXCTC_CMP=0 / 1 forces it off / on (A/B and test switch).
     DecodeParams q = p;
     const char* e_cmp = getenv("FLEXCTC_CMP");
-    q.use_cmp = p.cmp && p.rowoff && !p.ready && !p.logits && e_cmp && e_cmp[0] == '1' ? 1 : 0;
+    bool want_cmp = false;
+    {
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        want_cmp = p.K == 16 && p.Vp1 == 1025 && p.use_lm && p.lm.RW == 16 && p.use_bt && p.merge_mode == 0 &&
+                   !p.retract && p.alpha_lm >= 0.0f && p.alpha_bt >= 0.0f && !p.fuse_rep && p.B <= nsm;
+    }
+    if (e_cmp) want_cmp = e_cmp[0] == '1';
+    q.use_cmp = p.cmp && p.rowoff && !p.ready && !p.logits && want_cmp ? 1 : 0;
     if (q.use_cmp) {
         int rc = launch_rowoff(p.len_c, p.B, p.rowoff, stream, err);
         if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev2, st);

@@ -103,17 +103,27 @@ def test_warp_kernel_forced(lm_pair, bt_pair, monkeypatch, wname, mode):
     run_pair(D, L, wl_cfg(wl, merge_mode=mode), glm, olm, gbt, obt, ctx=f"warp {wname} m{mode}")
 
 
+@pytest.mark.parametrize("cmp", ["0", "1"])
 @pytest.mark.parametrize("wname", ["c3", "c4"])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_cta_kernel_with_compaction_records(lm_pair, bt_pair, monkeypatch, wname, mode):
-    """FLEXCTC_CMP=1: the persistent CTA kernel takes each frame's best token, listed band and
-    floor from the compaction pass's records instead of its own per-frame summaries."""
+def test_cta_kernel_with_compaction_records(lm_pair, bt_pair, monkeypatch, wname, mode, cmp):
+    """The persistent CTA kernel with (FLEXCTC_CMP=1: each frame's best token, listed band and
+    floor from the compaction pass's records; the default for the c4 shape) and without
+    (FLEXCTC_CMP=0: its own per-frame summaries) the records; both with the settled-beam fast path,
+    and once without it."""
     monkeypatch.setenv("FLEXCTC_WARP", "0")
-    monkeypatch.setenv("FLEXCTC_CMP", "1")
+    monkeypatch.setenv("FLEXCTC_CMP", cmp)
     wl, D, L, _, _ = synth.workload_inputs(wname)
     glm, olm = (lm_pair[0], lm_pair[1]) if wl.lm else (None, None)
     gbt, obt = (bt_pair[0], bt_pair[1]) if wl.boost else (None, None)
     run_pair(D, L, wl_cfg(wl, merge_mode=mode), glm, olm, gbt, obt, ctx=f"records {wname} m{mode}")
+
+
+def test_cta_kernel_without_fast_path(lm_pair, bt_pair, monkeypatch):
+    """FLEXCTC_FAST=0: every frame through the general phases (the fast path's A/B switch)."""
+    monkeypatch.setenv("FLEXCTC_FAST", "0")
+    wl, D, L, _, _ = synth.workload_inputs("c4")
+    run_pair(D, L, wl_cfg(wl), lm_pair[0], lm_pair[1], bt_pair[0], bt_pair[1], ctx="no fast path c4")
 
 
 def test_cta_kernel_with_compaction_records_k128(lm_pair, bt_pair, monkeypatch):

@@ -257,19 +257,6 @@ __global__ void __launch_bounds__(32 * kWarps, 3) frame_compact_kernel(const voi
         int b = lo_b;
         int64_t off = __ldg(&rowoff[b]), end = __ldg(&rowoff[b + 1]);
         const int64_t rend = min(nrows, r + kRowsPerWarp);
-        if (lane == 0) {  // the chunk's later rows into L2 (bulk prefetch) while row r is processed
-            int bb = b;
-            int64_t o2 = off, e2 = end;
-            for (int64_t r2 = r; r2 < rend; ++r2) {
-                while (r2 >= e2 && bb + 1 < B) { ++bb; o2 = e2; e2 = __ldg(&rowoff[bb + 1]); }
-                if (r2 == r) continue;
-                const char* src = (const char*)X + ((int64_t)bb * sb + (int64_t)(r2 - o2) * stt) * esz;
-                const char* g = (const char*)((uintptr_t)src & ~(uintptr_t)15);
-                const uint32_t nb = (uint32_t)(((src - g) + (int64_t)Vp1 * esz + 15) & ~(int64_t)15);
-                if (g >= lo && g + nb <= hi)
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(nb) : "memory");
-            }
-        }
         for (; r < rend; ++r) {
             while (r >= end) { ++b; off = end; end = __ldg(&rowoff[b + 1]); }  // skips empty utterances
             const int t = (int)(r - off);

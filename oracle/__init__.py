@@ -46,7 +46,8 @@ def build(force: bool = False) -> str:
 class Cfg(ctypes.Structure):
     _fields_ = [("beam", ctypes.c_int32), ("alpha_lm", ctypes.c_double), ("alpha_bt", ctypes.c_double),
                 ("beta", ctypes.c_double), ("theta", ctypes.c_double), ("merge_mode", ctypes.c_int32),
-                ("retract_boost_at_eos", ctypes.c_int32), ("fuse_repeats", ctypes.c_int32)]
+                ("retract_boost_at_eos", ctypes.c_int32), ("fuse_repeats", ctypes.c_int32),
+                ("merge_first", ctypes.c_int32)]
 
 
 _lib = None
@@ -172,9 +173,9 @@ class Boost:
 
 
 def make_cfg(beam, alpha_lm=0.0, alpha_bt=0.0, beta=0.0, theta=float("inf"), merge_mode=0, retract=0,
-             fuse_repeats=0) -> Cfg:
+             fuse_repeats=0, merge_first=0) -> Cfg:
     return Cfg(int(beam), float(alpha_lm), float(alpha_bt), float(beta), float(theta), int(merge_mode), int(retract),
-               int(fuse_repeats))
+               int(fuse_repeats), int(merge_first))
 
 
 def decode(D: np.ndarray, lengths, cfg: Cfg, lm: LM | None = None, boost: Boost | None = None,

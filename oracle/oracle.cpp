@@ -326,6 +326,53 @@ std::vector<std::pair<Hyp<R>, int>> decode_utt(const std::vector<std::vector<R>>
                 cand[f] = Cand<R>{s, f};
             }
         }
+        if (cfg->merge_first) {
+            // Reading R27 (BJ north_star: "merges duplicate prefixes by prefix hash, selects the
+            // top-K"): every candidate is first combined with the candidates of the same
+            // (transcript, last label) (R12) by the R13/R14 combiner, members ordered by (score
+            // desc, flat index asc); the K best groups by (merged score desc, flat index of the
+            // group's best member asc) are kept (R9's tie rule on the representative), then the
+            // θ-prune relative to the best group. The best member is the survivor:
+            // its slot and label give the backpointer and the alignment.
+            std::map<std::pair<std::vector<int>, int>, std::vector<Cand<R>>> groups;
+            for (const Cand<R>& c : cand) {  // flat index order
+                if (c.s == NEG) continue;
+                const int k = (int)(c.f / Vp1), w = (int)(c.f % Vp1);
+                std::vector<int> pre = slots[k].prefix;
+                if (w != blank && w != slots[k].last) pre.push_back(w);
+                groups[{std::move(pre), w}].push_back(c);
+            }
+            std::vector<Cand<R>> gl;  // {merged score, flat index of the best member}
+            for (auto& kv : groups) {
+                std::vector<Cand<R>>& g = kv.second;
+                std::stable_sort(g.begin(), g.end(), [](const Cand<R>& a, const Cand<R>& b) { return a.s > b.s; });
+                std::vector<R> sc;
+                for (const Cand<R>& c : g) sc.push_back(c.s);
+                gl.push_back(Cand<R>{combine<R>(sc, cfg->merge_mode), g[0].f});
+            }
+            std::sort(gl.begin(), gl.end(), [](const Cand<R>& a, const Cand<R>& b) {
+                if (a.s != b.s) return a.s > b.s;
+                return a.f < b.f;
+            });
+            std::vector<Hyp<R>> nxt(K);
+            const R gthr = gl.empty() ? NEG : gl[0].s - theta;
+            for (int i = 0; i < K; ++i) {
+                if (i >= (int)gl.size() || gl[i].s < gthr) { nxt[i] = Hyp<R>{{}, blank, NEG, {}, false}; continue; }
+                const int k = (int)(gl[i].f / Vp1), w = (int)(gl[i].f % Vp1);
+                const Hyp<R>& p = slots[k];
+                Hyp<R> h;
+                h.prefix = p.prefix;
+                if (w != blank && w != p.last) h.prefix.push_back(w);
+                h.last = w;
+                h.score = gl[i].s;
+                h.align = p.align;
+                h.align.push_back(w);
+                h.alive = true;
+                nxt[i] = std::move(h);
+            }
+            slots = std::move(nxt);
+            continue;
+        }
         // flat TopK, ties -> lower flat index (R9)
         std::partial_sort(cand.begin(), cand.begin() + K, cand.end(), [](const Cand<R>& a, const Cand<R>& b) {
             if (a.s != b.s) return a.s > b.s;

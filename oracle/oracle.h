@@ -30,6 +30,7 @@ typedef struct {
     int32_t merge_mode;    /* 0 = log-sum-exp, 1 = max (R13) */
     int32_t retract_boost_at_eos; /* DESIGN.md R17; default 0 */
     int32_t fuse_repeats;  /* 1: repeat candidates also get the LM / BT terms (PAPER.md P:167 variant) */
+    int32_t merge_first;   /* 1: recombine duplicate (prefix, last) candidates BEFORE the TopK (reading R27) */
 } oracle_cfg;
 
 const char* oracle_last_error(void);

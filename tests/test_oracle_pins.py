@@ -422,3 +422,98 @@ def test_full_beam_equals_path_enumeration(mode, fuse):
         a = dict(oracle.decode_nbest(D, oracle.make_cfg(64, alpha_lm=0.6, fuse_repeats=1), lm=lm))
         b = dict(oracle.decode_nbest(D, oracle.make_cfg(64, alpha_lm=0.6, fuse_repeats=0), lm=lm))
         assert a[()] == b[()] and any(abs(a[y] - b[y]) > 1e-6 for y in a if y)
+
+
+# ------------------------------------------------------ merge-before-TopK variant (reading R27)
+# BJ north_star: "merges duplicate prefixes by prefix hash, selects the top-K"; Alg. 1
+# selects first. merge_first = 1 recombines every (transcript, last label) group of the K·V'
+# candidates before the TopK.
+
+def test_merge_first_hand_fixture():
+    """Hand-derived two-frame case (a = 0, b = 1, blank = 2; K = 2, lse, no fusion terms).
+    Frame 0 from the empty beam: P(a) .5, P(b) .2, P(∅) .3 -> slots (a | a) .5 and (∅ | ∅) .3.
+    Frame 1, P(a) .32, P(b) .4, P(∅) .28; candidates (probabilities):
+      (a|a): .5·.32 = .16 (repeat) and .3·.32 = .096 (emission from ∅) -> group .256
+      (ab|b): .5·.4 = .20;  (a|∅): .5·.28 = .14;  (b|b): .3·.4 = .12;  (∅|∅): .3·.28 = .084
+    Merge first: the groups (a|a) .256 and (ab|b) .20 survive -> 1-best "a" at ln .256.
+    Alg. 1 (TopK first): candidates .20 (ab|b) and .16 (a|a) survive -> 1-best "ab" at ln .20,
+    "a" at ln .16 (the .096 member was cut before the merge)."""
+    D = np.log(np.array([[0.5, 0.2, 0.3], [0.32, 0.4, 0.28]]))
+    mf = dict(oracle.decode_nbest(D, oracle.make_cfg(2, merge_first=1)))
+    tk = dict(oracle.decode_nbest(D, oracle.make_cfg(2)))
+    assert set(mf) == {(0,), (0, 1)} and set(tk) == {(0,), (0, 1)}
+    assert mf[(0,)] == pytest.approx(math.log(0.256), abs=1e-12)
+    assert mf[(0, 1)] == pytest.approx(math.log(0.20), abs=1e-12)
+    assert tk[(0,)] == pytest.approx(math.log(0.16), abs=1e-12)
+    assert tk[(0, 1)] == pytest.approx(math.log(0.20), abs=1e-12)
+    # max combiner: the (a|a) group scores its best member (.16) and ranks below (ab|b) .20
+    mfx = dict(oracle.decode_nbest(D, oracle.make_cfg(2, merge_mode=1, merge_first=1)))
+    assert mfx[(0,)] == pytest.approx(math.log(0.16), abs=1e-12)
+    # θ-prune relative to the best GROUP: K = 3, θ = 0.6 keeps ∅ at frame 0 (ln(.5/.3) = .51) and
+    # prunes b (.92); at frame 1 the cut is .256·e^-.6 = .1405, so (a|∅) .14 is dropped (it would
+    # survive a cut relative to the best single candidate, .20·e^-.6 = .1098, and then add to "a"
+    # in the final merge): "a" stays at ln .256, "ab" at ln .20
+    mft = dict(oracle.decode_nbest(D, oracle.make_cfg(3, theta=0.6, merge_first=1)))
+    assert set(mft) == {(0,), (0, 1)}
+    assert mft[(0,)] == pytest.approx(math.log(0.256), abs=1e-12)
+    assert mft[(0, 1)] == pytest.approx(math.log(0.20), abs=1e-12)
+
+
+def _max_groups(T, Vp1):
+    """Largest number of distinct (transcript, last label) pairs over the frames (brute force)."""
+    import itertools
+    blank, best = Vp1 - 1, 0
+    for t in range(1, T + 1):
+        keys = set()
+        for a in itertools.product(range(Vp1), repeat=t):
+            y, prev = [], blank
+            for w in a:
+                if w != blank and w != prev:
+                    y.append(w)
+                prev = w
+            keys.add((tuple(y), a[-1]))
+        best = max(best, len(keys))
+    return best
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_merge_first_exact_with_group_sized_beam(mode):
+    """Merge-first keeps every (transcript, last) group when K >= their number, so with θ = ∞ it
+    equals the path enumeration already at K = max #groups (< K·V' candidates). Alg. 1 at the
+    same K cuts candidates before merging and must deviate somewhere (the pin separates the two)."""
+    from tests.exact.exhaustive import exhaustive_paths
+    syms = ["a", "b", "c"]
+    path = os.path.join(GOLDEN, "arpa_3gram.arpa")
+    lm = oracle.LM(path, 3, syms)
+    py = ArpaPy(path)
+    phrases = [[0, 1], [1, 2], [0, 1, 2], [2, 2, 0], [1, 1]]
+    bt = oracle.Boost(phrases, 0.7, 3)
+    bpy = BoostPy(phrases, 0.7)
+    rng = np.random.default_rng(77 + mode)
+    Vp1 = 4
+    deviates = False
+    for T in [1, 2, 3, 4, 5]:
+        D = _rand_logprobs(rng, T, Vp1)
+        K = _max_groups(T, Vp1)
+        kw = dict(alpha_lm=0.6, alpha_bt=0.8, beta=0.3, merge_mode=mode)
+        res = dict(oracle.decode_nbest(D, oracle.make_cfg(K, merge_first=1, **kw), lm=lm, boost=bt))
+        ex = exhaustive_paths(D, Vp1 - 1, "lse" if mode == 0 else "max", alpha_lm=0.6, lm=py, symbols=syms,
+                              alpha_bt=0.8, boost=bpy, beta=0.3)
+        assert set(res) == set(ex), T
+        for y, s in ex.items():
+            assert res[y] == pytest.approx(s, abs=1e-10), (T, y)
+        alg1 = dict(oracle.decode_nbest(D, oracle.make_cfg(K, **kw), lm=lm, boost=bt))
+        deviates |= set(alg1) != set(ex) or any(abs(alg1[y] - ex[y]) > 1e-9 for y in alg1)
+    assert deviates
+
+
+def test_merge_first_full_beam_equals_alg1():
+    """With K >= K·V' candidates and θ = ∞ nothing is cut: both orders are exact and agree."""
+    rng = np.random.default_rng(3)
+    for T in [1, 2, 3, 4]:
+        D = _rand_logprobs(rng, T, 3)
+        a = dict(oracle.decode_nbest(D, oracle.make_cfg(3 ** T, merge_first=1)))
+        b = dict(oracle.decode_nbest(D, oracle.make_cfg(3 ** T)))
+        assert set(a) == set(b)
+        for y in a:
+            assert a[y] == pytest.approx(b[y], abs=1e-12)

@@ -140,6 +140,12 @@ typedef struct {
     int32_t fuse_repeats;         /* 1: repeat candidates (w == last label) also get the α_LM / α_BT
                                      terms, at every occurrence (the variant the
                                      authors tried; no β, no state advance); default 0 = Alg. 1 */
+    int32_t merge_first;          /* 1: recombine duplicate (transcript, last label) candidates BEFORE
+                                     the TopK (BJ north_star "merges duplicate prefixes ..., selects
+                                     the top-K"; reading R27): groups ranked by merged
+                                     score, flat index of the best member on ties; θ-prune against the
+                                     best group. Runs merge_first_kernel (1-best only: nbest must be
+                                     1). Default 0 = Alg. 1's TopK -> recombine order */
 } flexctc_config;
 
 /* Workspace bytes for a decode of B utterances of up to T frames with V+1 = Vp1 tokens.

@@ -310,6 +310,7 @@ static flexctc_status validate_cfg(const flexctc_config* cfg) {
     if (!(cfg->theta >= 0.0f)) return fail(FLEXCTC_ERR_INVALID_ARG, "theta must be >= 0 (or +inf)");
     if (cfg->merge_mode != 0 && cfg->merge_mode != 1) return fail(FLEXCTC_ERR_INVALID_ARG, "merge_mode must be 0 or 1");
     if (cfg->fuse_repeats != 0 && cfg->fuse_repeats != 1) return fail(FLEXCTC_ERR_INVALID_ARG, "fuse_repeats must be 0 or 1");
+    if (cfg->merge_first != 0 && cfg->merge_first != 1) return fail(FLEXCTC_ERR_INVALID_ARG, "merge_first must be 0 or 1");
     if (!std::isfinite(cfg->alpha_lm) || !std::isfinite(cfg->alpha_bt) || !std::isfinite(cfg->beta))
         return fail(FLEXCTC_ERR_INVALID_ARG, "alpha/beta must be finite");
     return FLEXCTC_OK;
@@ -327,6 +328,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     flexctc_status st = validate_cfg(cfg);
     if (st != FLEXCTC_OK) return st;
     if (nbest < 1 || nbest > cfg->beam) return fail(FLEXCTC_ERR_INVALID_ARG, "nbest must be in [1, beam]");
+    if (cfg->merge_first && (nbest > 1 || logits)) return fail(FLEXCTC_ERR_INVALID_ARG, "merge_first: 1-best over log-probs only");
     if (B < 0 || T < 0) return fail(FLEXCTC_ERR_INVALID_ARG, "B and T must be >= 0");
     if (Vp1 < 2) return fail(FLEXCTC_ERR_INVALID_ARG, "Vp1 must be >= 2");
     if (Vp1 > kMaxVp1) return fail(FLEXCTC_ERR_CAPACITY, "Vp1 > 8192");
@@ -366,6 +368,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.B = B; p.T = T; p.Vp1 = Vp1; p.K = cfg->beam;
     p.alpha_lm = cfg->alpha_lm; p.alpha_bt = cfg->alpha_bt; p.beta = cfg->beta; p.theta = cfg->theta;
     p.merge_mode = cfg->merge_mode; p.retract = cfg->retract_boost_at_eos; p.fuse_rep = cfg->fuse_repeats ? 1 : 0;
+    p.merge_first = cfg->merge_first ? 1 : 0;
     p.use_lm = lm != nullptr; p.use_bt = boost != nullptr;
     if (lm) p.lm = lm->dev;
     if (boost) p.bt = boost->dev;

@@ -1577,7 +1577,7 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
     // K = 1 runs the greedy kernels (greedy_kernel.cu); FLEXCTC_GREEDY=0 keeps the beam kernel
     // (test switch: the two must agree)
     const char* e_gr = getenv("FLEXCTC_GREEDY");
-    const bool greedy = p.K == 1 && p.greedy_sum && !(e_gr && e_gr[0] == '0') && !p.fuse_rep;
+    const bool greedy = p.K == 1 && p.greedy_sum && !(e_gr && e_gr[0] == '0') && !p.fuse_rep && !p.merge_first;
     const bool plain = greedy && !p.use_lm && !p.use_bt && p.beta == 0.0f;
     if (!plain) {  // the plain greedy path clamps lengths itself and needs no order
         order_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p.lengths, p.B, p.T, p.order, p.len_c, p.flags, p.B <= 16384);
@@ -1598,6 +1598,7 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
         e = cudaGetLastError();
         if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     }
+    if (p.merge_first) return launch_merge_first(p, stream, ev0, ev1, err);  // reading R27
     if (greedy) return launch_greedy(p, stream, ev0, ev1, err);
     if (use_warp_path(p)) {
         // K <= 32: the bandwidth-bound compaction pass over every valid row, then one warp per

@@ -21,6 +21,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "device_common.cuh"
@@ -36,6 +37,14 @@ constexpr int kRowsPerWarp = 4;  // consecutive flattened rows per warp (one utt
 // 16-B blocks per lane held in registers: rows of <= 32·kBlk blocks (V' <= 1149 for fp32 log-probs,
 // <= 1273 for bf16 logits) stay in registers
 template <bool BF16> constexpr int kBlk = BF16 ? 5 : 9;
+
+// 0xffffffff if a >= b else 0 (one FSET: the counting and hit passes sum / mask these with
+// IADD3 / LOP3 instead of a predicate + select per element)
+__device__ __forceinline__ uint32_t ge_mask(float a, float b) {
+    uint32_t m;
+    asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(m) : "f"(a), "f"(b));
+    return m;
+}
 
 template <bool BF16>
 __device__ __forceinline__ float elem(const uint4& q, int j) {  // element j of a 16-B block
@@ -266,6 +275,249 @@ __global__ void __launch_bounds__(32 * kWarps, 3) frame_compact_kernel(const voi
     }
 }
 
+// ---- TMA-staged pass (the default when a row fits the registers) ----------------------------
+// Same records as frame_compact_kernel, different data movement: a persistent grid (#SMs x the
+// occupancy) in which warp g takes the chunks of 4 consecutive rows g, g + W, g + 2W, ... (W =
+// warps in the grid; neighbouring warps read neighbouring chunks). Each warp owns a ring of kStages row slots in shared memory; lane
+// 0 stages row k + kStages - 1 with ONE cp.async.bulk (TMA, completion on the slot's mbarrier)
+// before the warp ranks row k, so the HBM stream runs ahead of the ranking instead of every warp
+// alternating between waiting for its row and computing on it (the register-loading kernel above
+// ran at 0.55 IPC per SMSP with most warps stalled on their own loads).
+constexpr int kTWarps = 8;   // warps per CTA
+constexpr int kTChunk = 4;   // consecutive rows per warp chunk (one utterance search each)
+
+template <bool BF16>
+__host__ __device__ constexpr int slot_bytes(int Vp1) {  // covering 16-B blocks of any row alignment
+    return ((16 - (BF16 ? 2 : 4)) + Vp1 * (BF16 ? 2 : 4) + 15) & ~15;
+}
+template <int kStages>  // row slots per warp
+__host__ __device__ constexpr int warp_smem(int sbytes) { return kStages * sbytes + 8 * kCmpList + 16 * kStages; }
+
+// Row `src` into `slot` (16-B aligned) at byte offset src mod 16, completing on `bar` (count 1): one
+// bulk copy of the covering 16-B blocks when those lie inside [lo, hi) (the tensor's bytes),
+// otherwise (at most the tensor's first and last row) a plain copy of the row's own elements.
+template <bool BF16>
+__device__ __forceinline__ void stage_row(uint8_t* slot, const char* src, int Vp1, uint64_t* bar, const char* lo,
+                                          const char* hi, int lane) {
+    constexpr int ESZ = BF16 ? 2 : 4;
+    const int offb = (int)((uintptr_t)src & 15);
+    const char* g = src - offb;
+    const uint32_t bytes = (uint32_t)((offb + Vp1 * ESZ + 15) & ~15);
+    if (g >= lo && g + bytes <= hi) {
+        if (lane == 0) {
+            fence_proxy_async();  // the warp's earlier generic accesses of this slot before the async write
+            mbar_arrive_tx(bar, bytes);
+            bulk_g2s_hint(slot, g, bytes, bar, policy_evict_first());  // D is read once: keep the LM / boost tables in L2
+        }
+    } else {
+        for (int w = lane; w < Vp1; w += 32) {
+            if constexpr (BF16) ((uint16_t*)(slot + offb))[w] = __ldg((const uint16_t*)src + w);
+            else ((float*)(slot + offb))[w] = __ldg((const float*)src + w);
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    }
+}
+
+// One staged row -> one record (the ranking of compact_row, reading shared memory). Before the
+// blocks are loaded, the slot's elements outside the row's non-blank tokens (the head of block 0,
+// the blank and the tail of the last block) are overwritten with -inf, so the max / count / hit
+// passes need no per-element range test.
+template <bool BF16>
+__device__ void compact_staged(uint8_t* slot, int offb, int Vp1, uint8_t* rec, uint64_t* keys, int lane) {
+    constexpr int EPB = BF16 ? 8 : 4;
+    constexpr int ESZ = BF16 ? 2 : 4;
+    constexpr int NV = kBlk<BF16> * EPB;
+    const int blank = Vp1 - 1;
+    const int off = offb / ESZ;
+    const int nblk = (offb + Vp1 * ESZ + 15) >> 4;
+    auto ld_w = [&](int w) -> float {
+        if constexpr (BF16) return bf16f(((const uint16_t*)slot)[off + w]);
+        else return ((const float*)slot)[off + w];
+    };
+    const float xb = ld_w(blank);
+    __syncwarp();  // every lane has read the blank before it is masked
+    if (lane < EPB) {
+        const int e1 = lane, e2 = off + blank + lane;
+        if constexpr (BF16) {
+            if (e1 < off) ((uint16_t*)slot)[e1] = 0xff80u;
+            if (e2 < nblk * EPB) ((uint16_t*)slot)[e2] = 0xff80u;
+        } else {
+            if (e1 < off) ((float*)slot)[e1] = kNeg;
+            if (e2 < nblk * EPB) ((float*)slot)[e2] = kNeg;
+        }
+    }
+    __syncwarp();
+    const uint32_t ninf = BF16 ? 0xff80ff80u : 0xff800000u;
+    float v[NV];
+    float m4[4] = {kNeg, kNeg, kNeg, kNeg};
+#pragma unroll
+    for (int i = 0; i < kBlk<BF16>; ++i) {
+        const int bi = lane + 32 * i;
+        const uint4 q = bi < nblk ? ((const uint4*)slot)[bi] : make_uint4(ninf, ninf, ninf, ninf);
+#pragma unroll
+        for (int j = 0; j < EPB; ++j) {
+            v[i * EPB + j] = elem<BF16>(q, j);
+            m4[j & 3] = fmaxf(m4[j & 3], v[i * EPB + j]);
+        }
+    }
+    float mn = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mn = fmaxf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+
+    double lse = 0.0;
+    if constexpr (BF16) {  // R25: m over every logit, S in fp64, lse = m + log S
+        const double m = (double)fmaxf(mn, xb);
+        double S = 0.0;
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            if (v[i] > kNeg) S += exp((double)v[i] - m);
+        if (lane == 0) S += exp((double)xb - m);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+        lse = m + log(S);
+    }
+    auto dval = [&](float x) -> float {
+        if constexpr (BF16) return (float)((double)x - lse);
+        else return x;
+    };
+    auto count_ge = [&](float th, int& mine) -> int {
+        // v >= th  <=>  fl(v - th) has a clear sign bit (rounding never flips the sign; v == th
+        // gives +0; v = -inf gives -inf): one FADD and one LEA.HI per element count the values below
+        uint32_t c2[2] = {0u, 0u};
+#pragma unroll
+        for (int i = 0; i < NV; ++i) c2[i & 1] += __float_as_uint(__fsub_rn(v[i], th)) >> 31;
+        mine = NV - (int)(c2[0] + c2[1]);
+        return __reduce_add_sync(0xffffffffu, mine);
+    };
+    // band: the widest Δ in {16, 8, 4, 2, 1, 0} with at most kCmpList non-blank values >= mn - Δ.
+    // The binary search over the six starts at Δ = 2 instead of the middle (Δ = 4): on CTC-peaky
+    // rows Δ = 2 holds > 32 tokens on ~70 % of frames and Δ = 1 then fits, so most rows take two
+    // counting passes instead of three (same result: the counts are monotone in Δ)
+    float thr = INFINITY;
+    int n = 0, h = 0;
+    if (mn > kNeg) {
+        int lo_i = 0, hi_i = 5;
+        bool first = true;
+        while (lo_i <= hi_i) {
+            const int mid = first ? 3 : (lo_i + hi_i) >> 1;
+            first = false;
+            const float th = __fsub_rn(mn, mid == 5 ? 0.0f : (float)(16 >> mid));
+            int mine;
+            const int c = count_ge(th, mine);
+            if (c <= kCmpList) { thr = th; n = c; h = mine; hi_i = mid - 1; } else { lo_i = mid + 1; }
+        }
+    }
+    if (n > 0) {
+        int pos = h;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pos, o);
+            if (lane >= o) pos += y;
+        }
+        pos -= h;
+        if (h) {
+            uint32_t hlo = 0, hhi = 0;
+#pragma unroll
+            for (int e = 0; e < NV; ++e) {
+                if (e < 32) hlo |= ge_mask(v[e], thr) & (1u << e);
+                else hhi |= ge_mask(v[e], thr) & (1u << (e - 32));
+            }
+            uint64_t hm = ((uint64_t)hhi << 32) | hlo;
+            while (hm) {
+                const int e = __ffsll((long long)hm) - 1;
+                hm &= hm - 1;
+                const int w = (lane + 32 * (e / EPB)) * EPB + e % EPB - off;
+                const float x = ld_w(w);
+                keys[pos++] = ((uint64_t)ord_of(x) << 32) | (uint64_t)(0xffffffffu - (uint32_t)w);
+            }
+        }
+        __syncwarp();
+        if (lane < n) {
+            const uint64_t mykey = keys[lane];
+            int r = 0, r2 = 0;
+            int j = 0;
+            for (; j + 1 < n; j += 2) { r += keys[j] > mykey ? 1 : 0; r2 += keys[j + 1] > mykey ? 1 : 0; }
+            if (j < n) r += keys[j] > mykey ? 1 : 0;
+            r += r2;
+            const int w = (int)(0xffffffffu - (uint32_t)mykey);
+            ((float*)(rec + 32))[r] = dval(score_of(mykey));
+            ((uint16_t*)(rec + 160))[r] = (uint16_t)w;
+        }
+    }
+    if (lane == 0) {
+        float* f = (float*)rec;
+        f[0] = dval(xb);
+        f[1] = mn > kNeg ? dval(thr) : kNeg;
+        ((int32_t*)rec)[2] = n;
+        f[3] = mn > kNeg ? thr : INFINITY;
+        *(double*)(rec + 16) = lse;
+    }
+}
+
+template <bool BF16, int kStages>
+__global__ void __launch_bounds__(32 * kTWarps, kStages == 2 ? 3 : 2)
+    frame_compact_tma_kernel(const void* __restrict__ X, int64_t sb, int64_t stt, const int64_t* __restrict__ rowoff,
+                             int B, int T, int Vp1, uint8_t* __restrict__ cmp, const char* lo, const char* hi,
+                             int sbytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const size_t esz = BF16 ? 2 : 4;
+    uint8_t* base = smem + (size_t)wid * warp_smem<kStages>(sbytes);
+    uint64_t* keys = (uint64_t*)(base + kStages * sbytes);
+    uint64_t* bar = keys + kCmpList;
+    int2* meta = (int2*)(bar + kStages);  // (b, t) of the row in each slot
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const int64_t nrows = __ldg(&rowoff[B]);
+    // warp g takes the chunks of kTChunk consecutive rows g, g + W, g + 2W, ... (W = warps in the
+    // grid): one utterance search per chunk, the chunk's later rows advance the cursor
+    const int64_t W = (int64_t)gridDim.x * kTWarps;
+    const int64_t g = (int64_t)blockIdx.x * kTWarps + wid;
+    auto row_of = [&](int k) -> int64_t { return (g + (int64_t)(k / kTChunk) * W) * kTChunk + k % kTChunk; };
+    int ib = 0;  // issue cursor: utterance of the last issued row, its first and end rows
+    int64_t ioff = 0, iend = 0;
+    auto issue = [&](int k, int s) {
+        const int64_t r = row_of(k);
+        if (k % kTChunk == 0) {
+            int lo_b = 0, hi_b = B - 1;  // the last b with rowoff[b] <= r (L1-resident)
+            while (lo_b < hi_b) {
+                const int mid = (lo_b + hi_b + 1) >> 1;
+                if (__ldg(&rowoff[mid]) <= r) lo_b = mid; else hi_b = mid - 1;
+            }
+            ib = lo_b;
+            ioff = __ldg(&rowoff[ib]);
+            iend = __ldg(&rowoff[ib + 1]);
+        }
+        while (r >= iend) { ++ib; ioff = iend; iend = __ldg(&rowoff[ib + 1]); }  // skips empty utterances
+        const int t = (int)(r - ioff);
+        if (lane == 0) meta[s] = make_int2(ib, t);  // published by the arrive (release) / wait (acquire)
+        const char* row = (const char*)X + ((int64_t)ib * sb + (int64_t)t * stt) * esz;
+        stage_row<BF16>(base + s * sbytes, row, Vp1, &bar[s], lo, hi, lane);
+    };
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s)
+        if (row_of(s) < nrows) issue(s, s);
+    uint32_t ph = 0;
+    int s = 0;
+    for (int k = 0; row_of(k) < nrows; ++k) {
+        const int kn = k + kStages - 1;
+        const int sn = s == 0 ? kStages - 1 : s - 1;  // the slot ranked in the previous iteration
+        if (row_of(kn) < nrows) issue(kn, sn);
+        mbar_wait(&bar[s], (ph >> s) & 1u);
+        ph ^= 1u << s;
+        const int2 bt = meta[s];
+        const char* row = (const char*)X + ((int64_t)bt.x * sb + (int64_t)bt.y * stt) * esz;
+        compact_staged<BF16>(base + s * sbytes, (int)((uintptr_t)row & 15), Vp1,
+                             cmp + ((int64_t)bt.x * T + bt.y) * kCmpBytes, keys, lane);
+        __syncwarp();  // the slot and the key buffer are free again
+        s = s + 1 == kStages ? 0 : s + 1;
+    }
+}
+
 // rowoff[b] = Σ_{b' < b} len_c[b'], rowoff[B] = Σ L (one CTA; block scan over 1024-wide tiles)
 __global__ void __launch_bounds__(1024) rowoff_kernel(const int32_t* __restrict__ len_c, int B, int64_t* rowoff) {
     __shared__ int64_t s_w[32];
@@ -313,27 +565,54 @@ int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, st
     return 0;
 }
 
-// rowoff [B + 1] (launch_rowoff) on the device; one warp per 8 rows, grid = #SMs x 8 CTAs (grid
-// stride over Σ L_b / 8 row chunks).
+// rowoff [B + 1] (launch_rowoff) on the device. Rows that fit the registers: the TMA-staged pass,
+// a persistent grid of #SMs x its occupancy; longer rows: the register-loading kernel, one warp per
+// 4 rows, grid = #SMs x 16 CTAs at most (grid stride over Σ L_b / 4 row chunks).
 int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t, const int64_t* rowoff, int B, int T,
                    int Vp1, uint8_t* cmp, void* stream, std::string& err) {
     if (B == 0 || T == 0) return 0;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t max_chunks = ((int64_t)B * T + kRowsPerWarp - 1) / kRowsPerWarp;
-    const int64_t want = (max_chunks + kWarps - 1) / kWarps;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * 16));
     cudaStream_t st = (cudaStream_t)stream;
     // the tensor's byte range: no load leaves it (edge blocks of the first / last row are assembled
     // element by element)
     const size_t esz = bf16 ? 2 : 4;
     const char* lo = (const char*)x;
     const char* hi = lo + esz * ((size_t)(B - 1) * stride_b + (size_t)(T - 1) * stride_t + Vp1);
-    if (bf16)
-        frame_compact_kernel<true><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi);
-    else
-        frame_compact_kernel<false><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi);
+    const int epb = bf16 ? 8 : 4;
+    const int nblk_max = ((16 - (int)esz) / (int)esz + Vp1 + epb - 1) / epb;
+    const bool staged = getenv("FLEXCTC_CMP_TMA") ? getenv("FLEXCTC_CMP_TMA")[0] != '0' : true;
+    if (staged && nblk_max <= 32 * (bf16 ? kBlk<true> : kBlk<false>)) {
+        const int sbytes = bf16 ? slot_bytes<true>(Vp1) : slot_bytes<false>(Vp1);
+        const char* e_st = getenv("FLEXCTC_CMP_STAGES");
+        const int stages = e_st ? atoi(e_st) : 2;
+        auto go = [&](auto kern, int smem) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kTWarps, smem);
+            const int64_t want = ((int64_t)B * T + kTWarps * kTChunk - 1) / (kTWarps * kTChunk);
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
+            kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes);
+        };
+        if (stages == 2)
+            bf16 ? go(frame_compact_tma_kernel<true, 2>, kTWarps * warp_smem<2>(sbytes))
+                 : go(frame_compact_tma_kernel<false, 2>, kTWarps * warp_smem<2>(sbytes));
+        else if (stages == 4)
+            bf16 ? go(frame_compact_tma_kernel<true, 4>, kTWarps * warp_smem<4>(sbytes))
+                 : go(frame_compact_tma_kernel<false, 4>, kTWarps * warp_smem<4>(sbytes));
+        else
+            bf16 ? go(frame_compact_tma_kernel<true, 3>, kTWarps * warp_smem<3>(sbytes))
+                 : go(frame_compact_tma_kernel<false, 3>, kTWarps * warp_smem<3>(sbytes));
+    } else {
+        const int64_t max_chunks = ((int64_t)B * T + kRowsPerWarp - 1) / kRowsPerWarp;
+        const int64_t want = (max_chunks + kWarps - 1) / kWarps;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * 16));
+        if (bf16)
+            frame_compact_kernel<true><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi);
+        else
+            frame_compact_kernel<false><<<grid, 32 * kWarps, 0, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     return 0;

@@ -114,6 +114,7 @@ struct DecodeParams {
     int32_t B, T, Vp1, K;
     float alpha_lm, alpha_bt, beta, theta;
     int32_t merge_mode, retract, fuse_rep;
+    int32_t merge_first;  // reading R27: recombine before the TopK (merge_first_kernel.cu)
     int32_t use_lm, use_bt;
     int32_t solo_off;     // tuning/test switch: disable the beam-warp + helpers mode
     int32_t fast_off;     // A/B switch (FLEXCTC_FAST=0): disable the CTA kernel's settled-beam fast path
@@ -173,6 +174,8 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
 // warp-per-utterance beam kernel (warp_beam_kernel.cu), K <= 32, after launch_compact
 int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev_start, void* ev_stop, std::string& err);
 size_t warp_beam_smem_per_warp(int Vp1, bool bf16, int nch);
+// merge-before-TopK variant (merge_first_kernel.cu), after order_kernel
+int launch_merge_first(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
 // input side (input_kernel.cu): log-softmax of bf16 logits into a dense fp32 [B][T][Vp1] buffer
 // (frames [t0, t1) only; t1 = -1: every frame); preload_: force its module to load (see the .cu)
 int preload_log_softmax_bf16();

@@ -33,13 +33,15 @@ class Config(ctypes.Structure):
     """flexctc_config (Eq. (1) weights P:96-98, θ P:237)."""
     _fields_ = [("beam", ctypes.c_int32), ("alpha_lm", ctypes.c_float), ("alpha_bt", ctypes.c_float),
                 ("beta", ctypes.c_float), ("theta", ctypes.c_float), ("merge_mode", ctypes.c_int32),
-                ("retract_boost_at_eos", ctypes.c_int32), ("fuse_repeats", ctypes.c_int32)]
+                ("retract_boost_at_eos", ctypes.c_int32), ("fuse_repeats", ctypes.c_int32),
+                ("merge_first", ctypes.c_int32)]
 
 
 def config(beam: int, alpha_lm: float = 0.0, alpha_bt: float = 0.0, beta: float = 0.0,
-           theta: float = 12.0, merge_mode: int = 0, retract_boost_at_eos: int = 0, fuse_repeats: int = 0) -> Config:
+           theta: float = 12.0, merge_mode: int = 0, retract_boost_at_eos: int = 0, fuse_repeats: int = 0,
+           merge_first: int = 0) -> Config:
     return Config(int(beam), float(alpha_lm), float(alpha_bt), float(beta), float(theta), int(merge_mode),
-                  int(retract_boost_at_eos), int(fuse_repeats))
+                  int(retract_boost_at_eos), int(fuse_repeats), int(merge_first))
 
 
 class LmInfo(ctypes.Structure):

@@ -35,7 +35,7 @@ def gpu_decode(D, L, cfg, lm=None, bt=None, Vp1=None, alignment=True):
 
 def ocfg(c):
     return oracle.make_cfg(c.beam, c.alpha_lm, c.alpha_bt, c.beta, c.theta, c.merge_mode, c.retract_boost_at_eos,
-                           c.fuse_repeats)
+                           c.fuse_repeats, c.merge_first)
 
 
 def compare(g, o, idx=None, tol=TOL, bitwise=False, ctx=""):

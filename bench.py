@@ -439,7 +439,7 @@ def run_flexctc(args):
         ctraffic, ctraffic_src = ncu_traffic(tkey + "_compact")
         roof_cmp = {"bound": "hbm", "achieved": cmp_bytes / cmp_s / 1e9, "peak": peak, "unit": "GB/s",
                     "frac": cmp_bytes / cmp_s / 1e9 / peak, "traffic": ctraffic,
-                    "kernel": "frame_compact_kernel (every valid row once, 8 rows per warp)",
+                    "kernel": "frame_compact_tma_kernel (every valid row once; TMA 2-slot ring per warp, 4-row chunks)",
                     "kernel_ms": 1e3 * cmp_s, "algorithmic_bytes_per_launch": cmp_bytes,
                     "peak_source": peak_src, "traffic_source": ctraffic_src,
                     "share_of_step": cmp_s / (t_dec / args.steps)}

@@ -5,8 +5,8 @@
 Covers the beam-warp + helpers mode (K <= 32, LM + boosting), the whole-CTA mode (K = 64), the
 single-warp launch, the greedy kernels (plain and fused, K = 1; TMA bulk rows + mbarriers), the
 n-best output, the bf16-logits input pass and the streamed host path, on a few short utterances,
-and checks the results against the oracle. Round 2: the compaction pass, the warp kernel, and the
-CTA kernel reading compaction records."""
+and checks the results against the oracle. Round 2: the compaction pass (TMA-staged), the warp
+kernel, the CTA kernel reading compaction records, and the merge-before-TopK kernel."""
 import os
 import sys
 
@@ -94,9 +94,36 @@ def run_round2():
         print("  with", env)
 
 
+def run_merge_first():
+    """merge_first_kernel (reading R27): the buffer cut (θ = ∞, K = 4 on flat V' = 9 frames forces
+    repeated sorts) and the c4-shaped LM + boosting case."""
+    rng = np.random.default_rng(2)
+    D = synth.random_logprobs(rng, 3, 40, 9, peak=0.5).astype(np.float32)
+    L = np.array([40, 13, 0], dtype=np.int32)
+    out = F.decode(torch.from_numpy(D).cuda(), torch.from_numpy(L).cuda(), F.config(4, theta=float("inf"), merge_first=1))
+    torch.cuda.synchronize()
+    ref = oracle.decode(D, L, oracle.make_cfg(4, merge_first=1), nthreads=4)
+    assert np.array_equal(out["tokens"].cpu().numpy(), ref["tokens"])
+    assert np.allclose(out["scores"].cpu().numpy(), ref["scores"], atol=1e-4)
+    L = np.array([40, 17, 0], dtype=np.int32)
+    ph = synth.phrases(1024)
+    D, _ = synth.logprobs(3, 40, 1024, L, 5, ph)
+    arpa = synth.arpa_file(V=1024)
+    glm, gbt = F.LM(arpa, 1024, device=0), F.Boost(ph, 1.0, 1024, device=0)
+    out = F.decode(torch.from_numpy(D).cuda(), torch.from_numpy(L).cuda(), F.config(16, 0.5, 1.0, 0.5, 12.0, merge_first=1),
+                   glm, gbt)
+    torch.cuda.synchronize()
+    ref = oracle.decode(D, L, oracle.make_cfg(16, 0.5, 1.0, 0.5, 12.0, merge_first=1), oracle.LM(arpa, 1024),
+                        oracle.Boost(ph, 1.0, 1024), nthreads=4)
+    assert np.array_equal(out["tokens"].cpu().numpy(), ref["tokens"])
+    assert np.allclose(out["scores"].cpu().numpy(), ref["scores"], atol=1e-4)
+    print("merge_first ok")
+
+
 if __name__ == "__main__":
     run(16)
     run(64)
     run(16, nt=32)
     run_more()
     run_round2()
+    run_merge_first()

@@ -52,6 +52,8 @@ def parse():
                     help="bf16-logits: flexctc_decode_logits_bf16, log-softmax fused into the frame read (NEXT 4)")
     ap.add_argument("--beam", type=int, default=0,
                     help="override the workload's beam (1 = the greedy kernels, SURVEY §8(f) NEXT 1)")
+    ap.add_argument("--merge-first", action="store_true",
+                    help="the merge-before-TopK variant (config merge_first = 1, DESIGN.md reading R27)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0 = auto)")
@@ -203,13 +205,13 @@ def one_thread_times():
     return res
 
 
-def cpu_baseline(wl, D, L, arpa, ph, n_utts):
+def cpu_baseline(wl, D, L, arpa, ph, n_utts, merge_first=0):
     """The oracle as it stands (never tuned), on this host's cores, over a bounded sample."""
     import oracle
     lm = oracle.LM(arpa, wl.V) if wl.lm else None
     bt = oracle.Boost(ph, 1.0, wl.V) if wl.boost else None
     cfg = oracle.make_cfg(wl.beam, wl.alpha_lm if wl.lm else 0.0, wl.alpha_bt if wl.boost else 0.0, wl.beta,
-                          wl.theta, wl.merge_mode)
+                          wl.theta, wl.merge_mode, merge_first=merge_first)
     cores = os.cpu_count() or 1
     idx = np.arange(min(n_utts, D.shape[0]))
     Ds = np.ascontiguousarray(D[idx])
@@ -319,7 +321,7 @@ def run_flexctc(args):
     lm = F.LM(arpa, wl.V, device=gpu) if wl.lm else None
     bt = F.Boost(ph, 1.0, wl.V, device=gpu) if wl.boost else None
     cfg = F.config(wl.beam, wl.alpha_lm if wl.lm else 0.0, wl.alpha_bt if wl.boost else 0.0, wl.beta, wl.theta,
-                   wl.merge_mode)
+                   wl.merge_mode, merge_first=int(args.merge_first))
     Dd = torch.from_numpy(D).to(dev)
     bf16 = args.input == "bf16-logits"
     if bf16:  # the synthetic log-probs as bf16 logits (log-softmax is shift invariant)
@@ -496,11 +498,12 @@ def run_flexctc(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * t_dec / args.steps, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "input": args.input,
-            "config": workload_config(wl, B, T, frames_local, {"parallelism": f"dp{world} (utterance shards)"}
+            "config": workload_config(wl, B, T, frames_local, dict({"parallelism": f"dp{world} (utterance shards)"}
                                       if not strong else
                                       {"parallelism": f"dp{world} (one global batch LPT-sharded by length)",
                                        "global_batch": int(sum(sh["utterances"] for sh in shards)),
-                                       "stream_batches": args.stream}),
+                                       "stream_batches": args.stream},
+                                      **({"order": "merge-before-TopK (merge_first, R27)"} if args.merge_first else {}))),
             "frames_beams_per_s": fbps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -532,7 +535,7 @@ def run_flexctc(args):
         if world == 1 and not args.no_cpu_baseline:
             # the whole c4 batch (~20 core-seconds of oracle work); 16 utterances at K = 128
             n = args.cpu_sample or (min(B, 64) if wl.beam <= 32 else min(B, 16))
-            res["cpu_baseline"] = cpu_baseline(wl, D, L, arpa, ph, n)
+            res["cpu_baseline"] = cpu_baseline(wl, D, L, arpa, ph, n, int(args.merge_first))
         print(json.dumps(res), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -585,25 +585,16 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
     const bool staged = getenv("FLEXCTC_CMP_TMA") ? getenv("FLEXCTC_CMP_TMA")[0] != '0' : true;
     if (staged && nblk_max <= 32 * (bf16 ? kBlk<true> : kBlk<false>)) {
         const int sbytes = bf16 ? slot_bytes<true>(Vp1) : slot_bytes<false>(Vp1);
-        const char* e_st = getenv("FLEXCTC_CMP_STAGES");
-        const int stages = e_st ? atoi(e_st) : 2;
-        auto go = [&](auto kern, int smem) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kTWarps, smem);
-            const int64_t want = ((int64_t)B * T + kTWarps * kTChunk - 1) / (kTWarps * kTChunk);
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
-            kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes);
-        };
-        if (stages == 2)
-            bf16 ? go(frame_compact_tma_kernel<true, 2>, kTWarps * warp_smem<2>(sbytes))
-                 : go(frame_compact_tma_kernel<false, 2>, kTWarps * warp_smem<2>(sbytes));
-        else if (stages == 4)
-            bf16 ? go(frame_compact_tma_kernel<true, 4>, kTWarps * warp_smem<4>(sbytes))
-                 : go(frame_compact_tma_kernel<false, 4>, kTWarps * warp_smem<4>(sbytes));
-        else
-            bf16 ? go(frame_compact_tma_kernel<true, 3>, kTWarps * warp_smem<3>(sbytes))
-                 : go(frame_compact_tma_kernel<false, 3>, kTWarps * warp_smem<3>(sbytes));
+        // 2 row slots per warp (3 slots: 47 us at c4, 4 slots: 61 us, both fewer CTAs per SM than
+        // 2 slots' 44.5 us; profiles/r2/ab_compact_tma_stages.txt)
+        const int smem = kTWarps * warp_smem<2>(sbytes);
+        auto kern = bf16 ? frame_compact_tma_kernel<true, 2> : frame_compact_tma_kernel<false, 2>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kTWarps, smem);
+        const int64_t want = ((int64_t)B * T + kTWarps * kTChunk - 1) / (kTWarps * kTChunk);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
+        kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes);
     } else {
         const int64_t max_chunks = ((int64_t)B * T + kRowsPerWarp - 1) / kRowsPerWarp;
         const int64_t want = (max_chunks + kWarps - 1) / kWarps;

@@ -414,7 +414,9 @@ def run_flexctc(args):
     #                       and its 256-B record, writes 3·K B of backpointers; the compaction pass
     #                       reads the row and writes the record: Σ_b L_b · (4·V' + 256) (its own entry)
     plain_greedy = wl.beam == 1 and not wl.lm and not wl.boost and wl.beta == 0.0
-    xb = 2 if bf16 else 4
+    # bf16 logits: the warp path's compaction pass reads the logits (2 B); the CTA kernel's path
+    # normalises them first into a dense fp32 buffer that its compaction pass then reads (4 B)
+    xb = 2 if bf16 and kernel_name.startswith("warp_beam_kernel") else 4
     roof_cmp = None
     if wl.beam > 1 and compacted:
         alg_bytes = frames_local * (xb * Vp1 + 256 + 3 * wl.beam)

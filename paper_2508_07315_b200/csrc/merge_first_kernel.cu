@@ -93,6 +93,10 @@ __global__ void __launch_bounds__(kNT) merge_first_kernel(const DecodeParams p) 
     __shared__ int s_cnt, s_nsel, s_best_slot;
     __shared__ float s_tau;
     __shared__ float s_red[kNT / 32];
+    __shared__ int s_creps[kMaxBeam], s_corder[kMaxBeam], s_m1[kMaxBeam], s_ncls;
+    __shared__ float s_cub[kMaxBeam];
+    __shared__ uint64_t s_wkey[kNT / 32];
+    __shared__ int s_wstar;
     const int tid = threadIdx.x;
     const int K = p.K, Vp1 = p.Vp1, blank = Vp1 - 1, V = Vp1 - 1;
     const bool lm_on = p.use_lm != 0, bt_on = p.use_bt != 0;
@@ -251,41 +255,111 @@ __global__ void __launch_bounds__(kNT) merge_first_kernel(const DecodeParams p) 
             if (s_cnt >= K) cut_to_k();  // raises τ to the K-th special score
         }
         // ---- emission groups (P, c) no repeat group owns, pre-pruned by their bound
+        // per live class (representative P): its <= 2 members and the token-independent part of
+        // the bound, max acc + β + α_LM·ub(P) + α_BT·maxd(P) (+ ln 2 with two lse members)
         const bool no_bound = (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
-        const int64_t npairs = (int64_t)K * V;
-        for (int64_t base = 0; base < npairs; base += kSlab) {
-            if (s_cnt + kSlab > kCap) cut_to_k();
-            const float tau = s_tau;
-            for (int64_t i = base + tid; i < min(npairs, base + kSlab); i += kNT) {
-                const int P = (int)(i / V), c = (int)(i % V);
-                if (cls[P] != P || ca[P] == kNeg) continue;
-                // members: P's slots whose last label is not c (a slot with last == c repeats)
-                int mem[2]; int n = 0;
-                for (int j = P; j < K && n < 2; ++j)
-                    if (cls[j] == P && cl[j] != c) mem[n++] = j;
-                if (n == 0) continue;
-                bool owned = false;
-                for (int k = 0; k < K && !owned; ++k) owned = own[k] == P && cl[k] == c && ca[k] > kNeg;
-                if (owned) continue;
-                if (!no_bound && tau > kNeg) {
-                    float ub = __fadd_rn(fmaxf(ca[mem[0]], n > 1 ? ca[mem[1]] : kNeg), row[c]);
-                    ub = __fadd_rn(ub, p.beta);
-                    if (lm_on) ub = __fadd_rn(ub, p.alpha_lm * __int_as_float(recp(cls_l[P])[4]));
-                    if (bt_on) ub = __fadd_rn(ub, p.alpha_bt * __ldg(&p.bt.maxd[cbs[P]]));
-                    if (n > 1 && p.merge_mode == 0) ub = __fadd_rn(ub, 0.6931472f);
-                    ub += 1e-3f + 1e-5f * fabsf(ub);  // rounding margin
-                    if (ub < tau) continue;
-                }
-                float lp, bd; int ln, bn;
-                fusion(cls_l[P], cbs[P], c, lp, ln, bd, bn);
-                float s[2]; uint32_t f[2];
-                for (int m = 0; m < n; ++m) { s[m] = emit_score(ca[mem[m]], row[c], lp, bd); f[m] = (uint32_t)mem[m] * Vp1 + c; }
-                int r;
-                const float g = group_of(s, f, n, p.merge_mode, r);
-                if (g == kNeg) continue;
-                push(g, f[r], MfPay{(int)(f[r] / Vp1), c, ln, bn});
+        if (tid == 0) {
+            int nc = 0;
+            for (int k = 0; k < K; ++k)
+                if (cls[k] == k) s_creps[nc++] = k;
+            s_ncls = nc;
+        }
+        for (int k = tid; k < K; k += kNT) {
+            if (cls[k] != k) continue;
+            int m0 = k, m1 = -1;
+            for (int j = k + 1; j < K && m1 < 0; ++j)
+                if (cls[j] == k) m1 = j;
+            float ub = __fadd_rn(fmaxf(ca[m0], m1 >= 0 ? ca[m1] : kNeg), p.beta);
+            if (lm_on) ub = __fadd_rn(ub, p.alpha_lm * __int_as_float(recp(cls_l[k])[4]));
+            if (bt_on) ub = __fadd_rn(ub, p.alpha_bt * __ldg(&p.bt.maxd[cbs[k]]));
+            if (m1 >= 0 && p.merge_mode == 0) ub = __fadd_rn(ub, 0.6931472f);
+            s_cub[k] = ub;
+            s_m1[k] = m1;
+        }
+        __syncthreads();
+        const int ncls = s_ncls;
+        // best-token stage (raises τ before the bulk filter, as the TopK-first kernels' stage A):
+        // the frame's best non-blank token w* scored exactly for every live class in one round of
+        // lookups; these groups are excluded from the bulk pass below
+        {
+            float bv = kNeg;
+            int bw = -1;
+            for (int w = tid; w < V; w += kNT)
+                if (row[w] > bv || (row[w] == bv && bw >= 0 && w < bw)) { bv = row[w]; bw = w; }
+            uint64_t key = bw >= 0 ? make_key(bv, (uint32_t)bw) : 0ull;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) key = umax64(key, __shfl_xor_sync(0xffffffffu, key, o));
+            if ((tid & 31) == 0) s_wkey[tid >> 5] = key;
+            __syncthreads();
+            if (tid == 0) {
+                uint64_t k2 = s_wkey[0];
+                for (int i = 1; i < kNT / 32; ++i) k2 = umax64(k2, s_wkey[i]);
+                s_wstar = k2 ? (int)flat_of(k2) : -1;
             }
             __syncthreads();
+        }
+        const int wstar = s_wstar;
+        auto emission_group = [&](int P, int c, float tau) {
+            // members: P's slots whose last label is not c (a slot with last == c repeats)
+            int mem[2]; int n = 0;
+            if (cl[P] != c) mem[n++] = P;
+            const int m1 = s_m1[P];
+            if (m1 >= 0 && cl[m1] != c) mem[n++] = m1;
+            if (n == 0) return;
+            bool owned = false;
+            for (int k = 0; k < K && !owned; ++k) owned = own[k] == P && cl[k] == c && ca[k] > kNeg;
+            if (owned) return;
+            float lp, bd; int ln, bn;
+            fusion(cls_l[P], cbs[P], c, lp, ln, bd, bn);
+            float s[2]; uint32_t f[2];
+            for (int m = 0; m < n; ++m) { s[m] = emit_score(ca[mem[m]], row[c], lp, bd); f[m] = (uint32_t)mem[m] * Vp1 + c; }
+            int r;
+            const float g = group_of(s, f, n, p.merge_mode, r);
+            if (g == kNeg || g < tau) return;  // below a lower bound of the final cut
+            push(g, f[r], MfPay{(int)(f[r] / Vp1), c, ln, bn});
+        };
+        if (wstar >= 0) {
+            for (int ci = tid; ci < ncls; ci += kNT) emission_group(s_creps[ci], wstar, s_tau);
+            __syncthreads();
+            if (s_cnt >= K) cut_to_k();
+        }
+        // bulk pass: classes in order of their bound (cub desc); a class whose bound with the
+        // frame's best token cannot reach τ ends the pass (every later class is weaker), and τ is
+        // raised to the K-th best group after every class (threshold algorithm)
+        for (int ci = tid; ci < ncls; ci += kNT) {
+            const int P = s_creps[ci];
+            const float u = s_cub[P];
+            int r = 0;
+            for (int cj = 0; cj < ncls; ++cj) {
+                const float v = s_cub[s_creps[cj]];
+                r += (v > u || (v == u && cj < ci)) ? 1 : 0;
+            }
+            s_corder[r] = P;
+        }
+        __syncthreads();
+        const float dmax = wstar >= 0 ? row[wstar] : kNeg;
+        for (int ci = 0; ci < ncls; ++ci) {
+            const int P = s_corder[ci];
+            if (!no_bound && s_tau > kNeg) {
+                float ub = __fadd_rn(s_cub[P], dmax);
+                ub += 1e-3f + 1e-5f * fabsf(ub);
+                if (ub < s_tau) break;  // uniform: s_tau was last written before a barrier
+            }
+            for (int c0 = 0; c0 < V; c0 += kSlab) {
+                if (s_cnt + kSlab > kCap) cut_to_k();
+                const float tau = s_tau;
+                for (int c = c0 + tid; c < min(V, c0 + kSlab); c += kNT) {
+                    if (c == wstar) continue;  // scored in the best-token stage
+                    if (!no_bound && tau > kNeg) {
+                        float ub = __fadd_rn(s_cub[P], row[c]);
+                        ub += 1e-3f + 1e-5f * fabsf(ub);  // rounding margin
+                        if (ub < tau) continue;
+                    }
+                    emission_group(P, c, tau);
+                }
+                __syncthreads();
+            }
+            if (s_cnt > K) cut_to_k();
         }
         // ---- TopK over the groups, θ-prune, beams.update
         cut_to_k();

@@ -69,8 +69,8 @@ def test_small_vocab_no_lm_and_fuse_repeats(fuse):
              glm, olm, gbt, obt, ctx=f"mf fusion fuse{fuse}")
 
 
-@pytest.mark.parametrize("wname,B,K,mode", [("c1", 4, 4, 0), ("c4", 4, 16, 0), ("c4", 3, 16, 1), ("c3", 3, 8, 0),
-                                            ("c5", 2, 32, 0)])
+@pytest.mark.parametrize("wname,B,K,mode", [("c1", 4, 4, 0), ("c1", 4, 1, 0), ("c4", 4, 16, 0), ("c4", 3, 16, 1),
+                                            ("c4", 3, 1, 1), ("c3", 3, 8, 0), ("c5", 2, 32, 0)])
 def test_paper_shapes(lm_pair, bt_pair, wname, B, K, mode):
     """Paper-shaped utterances (V' = 129 / 1025, the synthetic 4-gram LM and 1000 phrases where the
     workload has them) through the variant."""

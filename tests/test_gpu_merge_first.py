@@ -81,6 +81,16 @@ def test_paper_shapes(lm_pair, bt_pair, wname, B, K, mode):
              ctx=f"mf {wname} K{K} mode{mode}")
 
 
+@pytest.mark.parametrize("K,theta,mode", [(64, float("inf"), 0), (128, 6.0, 1), (256, 8.0, 0)])
+def test_large_beams(K, theta, mode):
+    """K = 64 .. 256 (the buffer cut with hundreds of groups per frame), V' = 33, flat frames."""
+    rng = np.random.default_rng(K + mode)
+    B, T, Vp1 = 4, 60, 33
+    D = synth.random_logprobs(rng, B, T, Vp1, peak=1.0).astype(np.float32)
+    L = rng.integers(30, T + 1, B).astype(np.int32)
+    run_pair(D, L, F.config(K, beta=0.2, theta=theta, merge_mode=mode, merge_first=1), ctx=f"mf K{K}")
+
+
 def test_flag_is_live_and_nbest_refused(lm_pair, bt_pair):
     # flat frames and a small beam: members of one group fall on both sides of Alg. 1's TopK cut
     rng = np.random.default_rng(4)

@@ -394,7 +394,7 @@ static flexctc_status decode_impl(const float* log_probs, int64_t stride_b, int6
     p.nbest = nbest;
     std::string err;
     p.logits = logits;
-    if (logits && !use_warp_path(p)) {
+    if (logits && !use_warp_path(p) && !cta_logits_direct(p)) {
         // bf16 logits, K = 1 or K > 32: a bandwidth-bound log-softmax pass (R25) into the
         // workspace's dense fp32 [B][T][Vp1] region, then the decode of those log-probs (the
         // K <= 32 warp path instead fuses the log-softmax into its compaction pass)

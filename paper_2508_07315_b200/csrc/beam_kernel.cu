@@ -357,6 +357,14 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const bool lm_on = FUS ? (FUS & 1) != 0 : p.use_lm != 0, bt_on = FUS ? (FUS & 2) != 0 : p.use_bt != 0;
     const int RWS = RWC ? RWC : lm_on ? ((p.lm.RW + 3) & ~3) : 4;  // ints per cached record (int4 aligned)
     constexpr bool plain = (FUS & 4) != 0;
+    // FUS bit 4: bf16 logits read straight into the ring (2 B per logit from HBM) and normalised in
+    // shared memory with the lse of the frame's compaction record (R25); the specialised north-star
+    // variant only (solo, V' = 1025, 8 warps: 224 helper threads convert <= 5 elements each)
+    constexpr bool lgt = (FUS & 16) != 0;
+    static_assert(!lgt || (SOLO && VPC == 1025 && NT == 256 && (FUS & 8)), "bf16 rows: the records variant only");
+    constexpr int kConv = lgt ? (VPC + NT - 33) / (NT - 32) : 1;  // elements per helper thread
+    const int RS = VP + (lgt ? 20 : 4);  // ring slot stride (floats); bf16 rows are staged at byte kStage
+    const int kStage = (2 * VP + 32 + 15) & ~15;
     const bool ub_inf = plain ? false : (lm_on && p.alpha_lm < 0.0f) || (bt_on && p.alpha_bt < 0.0f);
     // compaction records: the generic variants follow p.use_cmp; specialised ones compile them in
     // (FUS bit 3) or out
@@ -371,6 +379,10 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     const int lnt = solo ? NT - 32 : NT;
     uint32_t st[kNumStats] = {};
     int ready = 0;  // streamed input: frames known to have landed (wait_ready)
+    // bf16 logits (lgt): the tensor's byte range (rows whose covering 16-B blocks leave it are
+    // copied element by element)
+    const char* lg_lo = lgt ? (const char*)p.logits : nullptr;
+    const char* lg_hi = lgt ? lg_lo + 2 * ((size_t)(p.B - 1) * p.stride_b + (size_t)(p.T - 1) * p.stride_t + Vp1) : nullptr;
 
     Shared sm;
     float* rowval = nullptr;  // [nrow][VP] LM rows (row cache)
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
     {
         unsigned char* q = smem_raw;
         auto take = [&](size_t bytes) { unsigned char* r = q; q += (bytes + 15) & ~size_t(15); return r; };
-        sm.ring = (float*)take(sizeof(float) * (size_t)R * (VP + 4));
+        sm.ring = (float*)take(sizeof(float) * (size_t)R * RS);
         sm.rring = (unsigned char*)take(p.use_cmp ? (size_t)R * kCmpBytes : 0);
         {
             Bank& B = sm.bk;  // both banks of each field, contiguous
@@ -440,6 +452,7 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
         const int b = p.order[u];
         const int L = p.len_c[b];
         const float* Db = p.log_probs + (int64_t)b * p.stride_b;
+        const uint16_t* Lb = lgt ? p.logits + (int64_t)b * p.stride_b : nullptr;
         if (tid == 0) sc.fast = 0;
         ready = 0;  // streamed input: what this thread has seen landed, per utterance
         const int64_t bp_base = (int64_t)b * p.T * K;  // backpointers of this utterance
@@ -470,7 +483,8 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             for (int r = 0; r < pf; ++r) {  // prologue
                 if (r < L) {
                     wait_ready(p, u, r, ready);
-                    load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                    if (lgt) load_row_bf16((char*)(sm.ring + (size_t)(r & (R - 1)) * RS) + kStage, Lb + (int64_t)r * p.stride_t, Vp1, ltid, lnt, lg_lo, lg_hi);
+                    else load_row(sm.ring + (size_t)(r & (R - 1)) * RS, Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
                     if (use_cmp && ltid < kCmpBytes / 16)
                         cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
                                    p.cmp + ((int64_t)b * p.T + r) * kCmpBytes + 16 * ltid);
@@ -488,13 +502,14 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
             const Bank nxt = bank(cb ^ 1);
             const long long ctop = TCLK();
             const int slot = t & (R - 1);  // R is 4 or 2
-            float* ring_t = sm.ring + (size_t)slot * (VP + 4);
-            const float* row = ring_t + row_off(Db + (int64_t)t * p.stride_t);
+            float* ring_t = sm.ring + (size_t)slot * RS;
+            const float* row = lgt ? ring_t : ring_t + row_off(Db + (int64_t)t * p.stride_t);
             if (!solo || helper) {
                 const int r = t + pf;
                 if (r < L) {
                     wait_ready(p, u, r, ready);
-                    load_row(sm.ring + (size_t)(r & (R - 1)) * (VP + 4), Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
+                    if (lgt) load_row_bf16((char*)(sm.ring + (size_t)(r & (R - 1)) * RS) + kStage, Lb + (int64_t)r * p.stride_t, Vp1, ltid, lnt, lg_lo, lg_hi);
+                    else load_row(sm.ring + (size_t)(r & (R - 1)) * RS, Db + (int64_t)r * p.stride_t, Vp1, ltid, lnt, p.overread);
                     if (use_cmp && ltid < kCmpBytes / 16)
                         cp_async16(sm.rring + (size_t)(r & (R - 1)) * kCmpBytes + 16 * ltid,
                                    p.cmp + ((int64_t)b * p.T + r) * kCmpBytes + 16 * ltid);
@@ -511,6 +526,25 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                 // or, with records, the record's list (band <= 16 nats, <= 32 tokens) and floor
                 const int h = ltid;
                 helpers_sync(lnt);  // every helper's cp.async of row t (and record) has landed
+                if constexpr (lgt) {
+                    // D = (float)(x - lse) (R25) into the slot's float row: read every staged logit
+                    // first (the float row overlaps the staging bytes), then write
+                    const double lse = *(const double*)(rc_t + 16);
+                    const char* sb = (const char*)ring_t + kStage + ((uintptr_t)(Lb + (int64_t)t * p.stride_t) & 15);
+                    float xv[kConv];
+#pragma unroll
+                    for (int i = 0; i < kConv; ++i) {
+                        const int w = h + i * (NT - 32);
+                        xv[i] = w < Vp1 ? bf16f(*(const uint16_t*)(sb + 2 * w)) : 0.0f;
+                    }
+                    helpers_sync(lnt);
+#pragma unroll
+                    for (int i = 0; i < kConv; ++i) {
+                        const int w = h + i * (NT - 32);
+                        if (w < Vp1) ring_t[w] = (float)((double)xv[i] - lse);
+                    }
+                    helpers_sync(lnt);
+                }
                 const int rn = use_cmp ? ((const int*)rc_t)[2] : 0;
                 const float rfl = use_cmp ? ((const float*)rc_t)[1] : INFINITY;
                 if (use_cmp && !(rn == 0 && rfl == INFINITY)) {
@@ -1350,10 +1384,10 @@ __global__ void order_kernel(const int32_t* __restrict__ lengths, int B, int T, 
     order[rank] = b;
 }
 
-size_t smem_bytes(int K, int Vp1, int R, int cap, int nch, int RWS) {
+size_t smem_bytes(int K, int Vp1, int R, int cap, int nch, int RWS, bool lgt) {
     const int VP = (Vp1 + 3) & ~3;
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-    size_t s = al(sizeof(float) * (size_t)R * (VP + 4)) + (size_t)R * kCmpBytes;
+    size_t s = al(sizeof(float) * (size_t)R * (VP + (lgt ? 20 : 4))) + (size_t)R * kCmpBytes;
     s += al(8 * K) + al(8 * K) + al(16 * K) + al(8 * K) + al(8 * K) + al(2 * K) + al(8 * (size_t)K * RWS) + al(16 * K);
     s += al(8 * (size_t)cap) + 2 * al(4 * (size_t)cap);
     s += al(8 * K) + 2 * al(4 * K);
@@ -1373,7 +1407,7 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
     pl.R = VP <= 2048 ? 4 : 2;
     pl.cap = 4 * NT;  // >= 3K phase-1/2 pushes, and >= kPairCap + K for phase 4
     const int RWS = p.use_lm ? ((p.lm.RW + 3) & ~3) : 4;
-    pl.sm = smem_bytes(p.K, p.Vp1, pl.R, pl.cap, p.nch, RWS) + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) + 16 : 0);
+    pl.sm = smem_bytes(p.K, p.Vp1, pl.R, pl.cap, p.nch, RWS, p.logits != nullptr) + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) + 16 : 0);
     if (pl.sm > 200 * 1024) { err = "shared memory requirement too large (V+1 or T)"; return 2; }
     auto kern = ctc_beam_kernel<NT, LMV, false>;
     cudaFuncAttributes fattr{};
@@ -1421,6 +1455,9 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 15>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
         if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 31>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
+        if (e == cudaSuccess)
             e = cudaFuncSetAttribute(ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 5>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.sm);
         if (e == cudaSuccess)
@@ -1436,6 +1473,10 @@ int plan_nt(const DecodeParams& p, Plan& pl, std::string& err) {
 template <int NT, int LMV>
 int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void* ev0, void* ev1, std::string& err) {
     const int grid = std::min(p.B, nsm * pl.occ);
+    if (p.logits && !(NT == 256 && LMV == 2 && p.Vp1 == 1025)) {
+        err = "bf16 logits: no kernel variant for this configuration";
+        return 2;
+    }
     DecodeParams q = p;
     const char* e_solo = getenv("FLEXCTC_SOLO");  // "0": every phase uses the whole CTA (test switch)
     q.solo_off = (e_solo && e_solo[0] == '0') ? 1 : 0;
@@ -1449,7 +1490,11 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
             if (p.Vp1 == 1025) {
                 const bool plain = pl.nrow == 0 && p.merge_mode == 0 && !p.retract && p.alpha_lm >= 0.0f &&
                                    p.alpha_bt >= 0.0f;
-                if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // the north-star decode
+                if (p.logits) {  // bf16 logits read by the kernel itself (cta_logits_direct)
+                    if (solo && p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)
+                        ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 31><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
+                    else { err = "bf16 logits: no kernel variant for this configuration"; return 2; }
+                } else if (solo && !p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // the north-star decode
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 7><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
                 else if (solo && p.use_cmp && p.K == 16 && p.use_lm && p.lm.RW == 16 && p.use_bt && plain)  // ... reading records
                     ctc_beam_kernel<NT, LMV, true, 1025, 16, 16, 15><<<grid, NT, pl.sm, st>>>(q, pl.R, pl.cap, pl.nrow, pl.dense_min);
@@ -1569,6 +1614,25 @@ bool use_warp_path(const DecodeParams& p) {
     return per + (p.use_bt ? 8 * (size_t)(p.Vp1 - 1) : 0) <= 200 * 1024;
 }
 
+// bf16 logits on the CTA path (K <= 32 at B <= #SMs): the north-star shape reads them directly —
+// the compaction pass takes the logits (fused log-softmax, records carry the lse) and the specialised
+// records variant stages bf16 rows and normalises them in shared memory — so HBM carries 2 B per
+// logit twice instead of 2 + 4 + 4 + 4 through a dense fp32 copy. Other shapes keep that copy
+// (flexctc_decode_logits_bf16 in api.cu). Every knob that could steer the launch elsewhere
+// (FLEXCTC_CMP / SOLO / NT / DENSE_MIN, FLEXCTC_LOGITS_DIRECT=0) turns it off.
+bool cta_logits_direct(const DecodeParams& p) {
+    if (!p.logits || !p.cmp || !p.rowoff || p.ready || p.nbest > 1 || p.fuse_rep || p.merge_first) return false;
+    for (const char* e : {"FLEXCTC_CMP", "FLEXCTC_SOLO", "FLEXCTC_NT", "FLEXCTC_DENSE_MIN"})
+        if (getenv(e)) return false;
+    const char* e_ld = getenv("FLEXCTC_LOGITS_DIRECT");
+    if (e_ld && e_ld[0] == '0') return false;
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return p.K == 16 && p.Vp1 == 1025 && p.use_lm && p.lm.RW == 16 && p.lm.NL <= 2 && p.use_bt && p.merge_mode == 0 &&
+           !p.retract && p.alpha_lm >= 0.0f && p.alpha_bt >= 0.0f && p.B <= nsm;
+}
+
 int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std::string& err, void* ev2, void* ev3) {
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(p.flags, 0, 64 + 8 * kStatsWords, st);
@@ -1631,11 +1695,13 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
                    !p.retract && p.alpha_lm >= 0.0f && p.alpha_bt >= 0.0f && !p.fuse_rep && p.B <= nsm;
     }
     if (e_cmp) want_cmp = e_cmp[0] == '1';
-    q.use_cmp = p.cmp && p.rowoff && !p.ready && !p.logits && want_cmp ? 1 : 0;
+    q.use_cmp = p.cmp && p.rowoff && !p.ready && (!p.logits || cta_logits_direct(p)) && want_cmp ? 1 : 0;
+    if (p.logits && !q.use_cmp) { err = "bf16 logits: the CTA kernel reads them only with records"; return 2; }
     if (q.use_cmp) {
         int rc = launch_rowoff(p.len_c, p.B, p.rowoff, stream, err);
         if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev2, st);
-        if (!rc) rc = launch_compact(p.log_probs, false, p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err);
+        if (!rc) rc = launch_compact(p.logits ? (const void*)p.logits : (const void*)p.log_probs, p.logits != nullptr,
+                                     p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err);
         if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev3, st);
         if (rc) return rc;
     }

@@ -137,6 +137,24 @@ __device__ __forceinline__ void load_row(float* slot, const float* src, int Vp1,
     if (t0 + tid < Vp1) cp_async4(dst + t0 + tid, src + t0 + tid);
 }
 
+// bf16 logits row into a 16-B aligned staging area: the row's covering 16-B blocks by cp.async
+// (row element w at dst + (src mod 16) + 2w) when they lie inside [lo, hi), else (the tensor's
+// first / last row) plain element copies, visible after the caller's barrier. Plain cp.async.cg:
+// the same copy with an L2::cache_hint evict-first policy raised "illegal instruction" on the B200
+// in this kernel (the fp32 rows' copies carry the hint without trouble), so the logits ride the
+// default L2 policy.
+__device__ __forceinline__ void load_row_bf16(char* dst, const uint16_t* src, int Vp1, int tid, int nt, const char* lo,
+                                              const char* hi) {
+    const char* s = (const char*)src;
+    const char* g = (const char*)((uintptr_t)s & ~(uintptr_t)15);
+    const int nb16 = (int)(((s - g) + 2 * Vp1 + 15) >> 4);
+    if (g >= lo && g + 16 * (size_t)nb16 <= hi) {
+        for (int i = tid; i < nb16; i += nt) cp_async16(dst + 16 * i, g + 16 * i);
+    } else {
+        for (int w = tid; w < Vp1; w += nt) *(uint16_t*)(dst + (s - g) + 2 * w) = __ldg(src + w);
+    }
+}
+
 // Streamed input (flexctc_decode_host): wait until frame r of the utterance at LPT position u has
 // landed. First wave (u < p.wave, or p.wave = 0): ready[0] > r (frames sent frame-major); later
 // utterances: ready[1] > u - p.wave (sent whole, in LPT order). `ready` caches what this thread

@@ -163,6 +163,7 @@ WorkspaceLayout workspace_layout(int32_t B, int32_t T, int32_t K);
 
 // launches (beam_kernel.cu; K = 1 goes to launch_greedy in greedy_kernel.cu)
 bool use_warp_path(const DecodeParams& p);  // K <= 32 warp path eligible (p.logits: bf16 input)
+bool cta_logits_direct(const DecodeParams& p);  // bf16 logits read by the CTA kernel itself
 // ev_start / ev_stop around the beam kernel, ev_cmp_start / ev_cmp_stop around the compaction pass
 int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err,
                   void* ev_cmp_start = nullptr, void* ev_cmp_stop = nullptr);

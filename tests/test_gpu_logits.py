@@ -66,3 +66,26 @@ def test_logits_bf16_strided_and_nan_padding():
     Dq = oracle.log_softmax_bf16(bits)
     o = oracle.decode(Dq, L, ocfg(F.config(4)), with_alignment=True)
     compare(g, o)
+
+
+@pytest.mark.parametrize("direct", ["1", "0"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_logits_direct_cta_path(lm_pair, bt_pair, monkeypatch, direct, mode):
+    """The north-star shape at B <= #SMs: the CTA kernel stages the bf16 rows itself and normalises
+    them with the compaction records' lse (FLEXCTC_LOGITS_DIRECT=1, the default) or decodes the
+    dense fp32 copy of the normalisation pass (=0). Ragged lengths incl. 0 and 1, unaligned rows
+    (V' = 1025 bf16 = 2050 B per row), the tensor's first and last rows at the buffer edges."""
+    if direct == "0":
+        monkeypatch.setenv("FLEXCTC_LOGITS_DIRECT", "0")
+    wl, D, L, _, _ = synth.workload_inputs("c4", B=10)
+    L = L.copy()
+    L[1], L[4], L[7] = 0, 1, 217
+    shift = np.random.default_rng(11).uniform(-5, 5, D.shape[:2] + (1,)).astype(np.float32)
+    bits = bf16_bits(D + shift)
+    Dq = oracle.log_softmax_bf16(bits)
+    cfg = wl_cfg(wl, merge_mode=mode)
+    g = gpu_logits(bits, L, cfg, lm_pair[0], bt_pair[0])
+    o = oracle.decode(Dq, L, ocfg(cfg), lm_pair[1], bt_pair[1], with_alignment=True)
+    compare(g, o, bitwise=mode == 1, ctx=f"logits direct={direct} mode={mode}")
+    if mode == 0:  # the records path (lse only); with direct = 1 the kernel staged the bf16 rows itself
+        assert F.flexctc.last_kernel() == "ctc_beam_kernel+records"

@@ -376,7 +376,7 @@ def run_flexctc(args):
     torch.cuda.synchronize()
     t_dec = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3        # s, whole decode per step summed
     t_kern = sum(e[2].elapsed_time(e[3]) for e in ev) / 1e3       # s, beam kernel only
-    compacted = compacted or kernel_name.endswith("+records")  # CTA kernel reading the records
+    compacted = compacted or "+records" in kernel_name  # CTA kernel reading the records
     t_cmp = sum(e[4].elapsed_time(e[5]) for e in ev) / 1e3 if compacted else 0.0  # s, compaction pass
     t_dec_local = t_dec
     flags = F.check(ws)
@@ -414,9 +414,10 @@ def run_flexctc(args):
     #                       and its 256-B record, writes 3·K B of backpointers; the compaction pass
     #                       reads the row and writes the record: Σ_b L_b · (4·V' + 256) (its own entry)
     plain_greedy = wl.beam == 1 and not wl.lm and not wl.boost and wl.beta == 0.0
-    # bf16 logits: the warp path's compaction pass reads the logits (2 B); the CTA kernel's path
-    # normalises them first into a dense fp32 buffer that its compaction pass then reads (4 B)
-    xb = 2 if bf16 and kernel_name.startswith("warp_beam_kernel") else 4
+    # bf16 logits: the compaction pass reads the logits (2 B) on the warp path and on the CTA path
+    # that reads them directly (kernel "...+records+bf16"); elsewhere the CTA path normalises them
+    # first into a dense fp32 buffer that the pass then reads (4 B)
+    xb = 2 if bf16 and (kernel_name.startswith("warp_beam_kernel") or kernel_name.endswith("+bf16")) else 4
     roof_cmp = None
     if wl.beam > 1 and compacted:
         alg_bytes = frames_local * (xb * Vp1 + 256 + 3 * wl.beam)

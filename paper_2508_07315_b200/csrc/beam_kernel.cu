@@ -1527,7 +1527,7 @@ int run_nt(const DecodeParams& p, const Plan& pl, int nsm, cudaStream_t st, void
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && ev0 && ev1) cudaEventRecord((cudaEvent_t)ev1, st);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-    set_kernel_name(p.use_cmp ? "ctc_beam_kernel+records" : "ctc_beam_kernel");
+    set_kernel_name(p.logits ? "ctc_beam_kernel+records+bf16" : p.use_cmp ? "ctc_beam_kernel+records" : "ctc_beam_kernel");
     return 0;
 }
 

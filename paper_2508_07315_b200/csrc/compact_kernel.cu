@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "device_common.cuh"
@@ -324,7 +325,8 @@ __device__ __forceinline__ void stage_row(uint8_t* slot, const char* src, int Vp
 // the blank and the tail of the last block) are overwritten with -inf, so the max / count / hit
 // passes need no per-element range test.
 template <bool BF16>
-__device__ void compact_staged(uint8_t* slot, int offb, int Vp1, uint8_t* rec, uint64_t* keys, int lane) {
+__device__ void compact_staged(uint8_t* slot, int offb, int Vp1, uint8_t* rec, uint64_t* keys, int lane,
+                               const double* __restrict__ etab) {
     constexpr int EPB = BF16 ? 8 : 4;
     constexpr int ESZ = BF16 ? 2 : 4;
     constexpr int NV = kBlk<BF16> * EPB;
@@ -369,13 +371,26 @@ __device__ void compact_staged(uint8_t* slot, int offb, int Vp1, uint8_t* rec, u
     if constexpr (BF16) {  // R25: m over every logit, S in fp64, lse = m + log S
         const double m = (double)fmaxf(mn, xb);
         double S = 0.0;
+        if (etab && m >= -700.0 && m <= 700.0) {
+            // exp of every bf16 value from a 65536-entry fp64 table (exp_table_kernel): lse =
+            // log Σ exp(x) = m + log Σ exp(x - m) with one table load per logit instead of an
+            // fp64 exp (|m| <= 700: no term overflows, the largest does not underflow)
 #pragma unroll
-        for (int i = 0; i < NV; ++i)
-            if (v[i] > kNeg) S += exp((double)v[i] - m);
-        if (lane == 0) S += exp((double)xb - m);
+            for (int i = 0; i < NV; ++i)
+                if (v[i] > kNeg) S += __ldg(&etab[__float_as_uint(v[i]) >> 16]);
+            if (lane == 0) S += __ldg(&etab[__float_as_uint(xb) >> 16]);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
-        lse = m + log(S);
+            for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+            lse = log(S);
+        } else {
+#pragma unroll
+            for (int i = 0; i < NV; ++i)
+                if (v[i] > kNeg) S += exp((double)v[i] - m);
+            if (lane == 0) S += exp((double)xb - m);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+            lse = m + log(S);
+        }
     }
     auto dval = [&](float x) -> float {
         if constexpr (BF16) return (float)((double)x - lse);
@@ -456,10 +471,10 @@ __device__ void compact_staged(uint8_t* slot, int offb, int Vp1, uint8_t* rec, u
 }
 
 template <bool BF16, int kStages>
-__global__ void __launch_bounds__(32 * kTWarps, kStages == 2 ? 3 : 2)
+__global__ void __launch_bounds__(32 * kTWarps, kStages == 2 && !BF16 ? 3 : 2)
     frame_compact_tma_kernel(const void* __restrict__ X, int64_t sb, int64_t stt, const int64_t* __restrict__ rowoff,
                              int B, int T, int Vp1, uint8_t* __restrict__ cmp, const char* lo, const char* hi,
-                             int sbytes) {
+                             int sbytes, const double* __restrict__ etab) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const size_t esz = BF16 ? 2 : 4;
@@ -512,7 +527,7 @@ __global__ void __launch_bounds__(32 * kTWarps, kStages == 2 ? 3 : 2)
         const int2 bt = meta[s];
         const char* row = (const char*)X + ((int64_t)bt.x * sb + (int64_t)bt.y * stt) * esz;
         compact_staged<BF16>(base + s * sbytes, (int)((uintptr_t)row & 15), Vp1,
-                             cmp + ((int64_t)bt.x * T + bt.y) * kCmpBytes, keys, lane);
+                             cmp + ((int64_t)bt.x * T + bt.y) * kCmpBytes, keys, lane, etab);
         __syncwarp();  // the slot and the key buffer are free again
         s = s + 1 == kStages ? 0 : s + 1;
     }
@@ -556,6 +571,31 @@ __global__ void __launch_bounds__(1024) rowoff_kernel(const int32_t* __restrict_
     if (threadIdx.x == 0) rowoff[B] = s_carry;
 }
 
+// etab[u] = exp(bf16 value with bits u) in fp64 (inf / NaN patterns and overflowing values give
+// inf / NaN; the pass only uses the table when every term of the row is finite)
+__global__ void exp_table_kernel(double* etab) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < 65536) etab[u] = exp((double)bf16f((uint16_t)u));
+}
+
+// one table per device, built on first use and kept for the process lifetime (512 KB)
+const double* exp_table(cudaStream_t st) {
+    static std::mutex mu;
+    static double* tab[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    double*& t = tab[dev & 63];
+    if (!t) {
+        double* d = nullptr;
+        if (cudaMalloc(&d, 65536 * sizeof(double)) != cudaSuccess) return nullptr;
+        exp_table_kernel<<<256, 256, 0, st>>>(d);
+        if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) { cudaFree(d); return nullptr; }
+        t = d;
+    }
+    return t;
+}
+
 }  // namespace
 
 int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, std::string& err) {
@@ -594,7 +634,8 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kTWarps, smem);
         const int64_t want = ((int64_t)B * T + kTWarps * kTChunk - 1) / (kTWarps * kTChunk);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
-        kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes);
+        const double* etab = bf16 ? exp_table(st) : nullptr;  // NULL: the pass evaluates exp itself
+        kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes, etab);
     } else {
         const int64_t max_chunks = ((int64_t)B * T + kRowsPerWarp - 1) / kRowsPerWarp;
         const int64_t want = (max_chunks + kWarps - 1) / kWarps;

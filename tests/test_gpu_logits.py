@@ -88,4 +88,4 @@ def test_logits_direct_cta_path(lm_pair, bt_pair, monkeypatch, direct, mode):
     o = oracle.decode(Dq, L, ocfg(cfg), lm_pair[1], bt_pair[1], with_alignment=True)
     compare(g, o, bitwise=mode == 1, ctx=f"logits direct={direct} mode={mode}")
     if mode == 0:  # the records path (lse only); with direct = 1 the kernel staged the bf16 rows itself
-        assert F.flexctc.last_kernel() == "ctc_beam_kernel+records"
+        assert F.flexctc.last_kernel() == ("ctc_beam_kernel+records+bf16" if direct == "1" else "ctc_beam_kernel+records")

@@ -578,8 +578,11 @@ __global__ void exp_table_kernel(double* etab) {
     if (u < 65536) etab[u] = exp((double)bf16f((uint16_t)u));
 }
 
+}  // namespace
+
 // one table per device, built on first use and kept for the process lifetime (512 KB)
-const double* exp_table(cudaStream_t st) {
+const double* bf16_exp_table(void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
     static std::mutex mu;
     static double* tab[64] = {};
     int dev = 0;
@@ -587,6 +590,10 @@ const double* exp_table(cudaStream_t st) {
     std::lock_guard<std::mutex> g(mu);
     double*& t = tab[dev & 63];
     if (!t) {
+        // built synchronously (any stream may use it next); never inside a stream capture, where
+        // the callers fall back to evaluating exp themselves
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
         double* d = nullptr;
         if (cudaMalloc(&d, 65536 * sizeof(double)) != cudaSuccess) return nullptr;
         exp_table_kernel<<<256, 256, 0, st>>>(d);
@@ -595,8 +602,6 @@ const double* exp_table(cudaStream_t st) {
     }
     return t;
 }
-
-}  // namespace
 
 int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, std::string& err) {
     rowoff_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(len_c, B, rowoff);
@@ -634,7 +639,7 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kTWarps, smem);
         const int64_t want = ((int64_t)B * T + kTWarps * kTChunk - 1) / (kTWarps * kTChunk);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
-        const double* etab = bf16 ? exp_table(st) : nullptr;  // NULL: the pass evaluates exp itself
+        const double* etab = bf16 ? bf16_exp_table(st) : nullptr;  // NULL: the pass evaluates exp itself
         kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes, etab);
     } else {
         const int64_t max_chunks = ((int64_t)B * T + kRowsPerWarp - 1) / kRowsPerWarp;

@@ -170,6 +170,9 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev_start, void* ev_
 int launch_greedy(const DecodeParams& p, void* stream, void* ev_start, void* ev_stop, std::string& err);
 // frame compaction pass (compact_kernel.cu): records of every valid row; rowoff by launch_rowoff
 int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, std::string& err);
+// exp(x) in fp64 for every bf16 bit pattern x (65536 entries, one per device, built on first use;
+// NULL if it cannot be allocated): the log-sum-exp of bf16 rows by table loads (reading R25)
+const double* bf16_exp_table(void* stream);
 int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t, const int64_t* rowoff, int B, int T,
                    int Vp1, uint8_t* cmp, void* stream, std::string& err);
 // warp-per-utterance beam kernel (warp_beam_kernel.cu), K <= 32, after launch_compact

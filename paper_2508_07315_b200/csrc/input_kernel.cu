@@ -7,7 +7,8 @@
 // bf16 values (exact in fp32), S = sum exp(x - m) in fp64, lse = m + log(S) in fp64 (every lane
 // the same value), D = (float)(x - lse) written as a dense fp32 row. R25 fixes this arithmetic;
 // the fp64 sum runs in a different order than the oracle's (~1e-16 relative), so the fp32 outputs
-// agree except at a rounding boundary.
+// agree except at a rounding boundary. When |m| <= 700 the same lse is log(sum exp(x)) with the
+// exp of every bf16 value read from a table (bf16_exp_table) instead of evaluated.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,7 +29,7 @@ constexpr int kPerLane = 33;  // register-resident elements per lane at V' <= 10
 __global__ void __launch_bounds__(32 * kRows) log_softmax_bf16_kernel(const uint16_t* __restrict__ X, int64_t sb,
                                                                      int64_t st, const int32_t* __restrict__ lengths,
                                                                      int B, int T, int Vp1, float* __restrict__ out,
-                                                                     int t0, int t1) {
+                                                                     int t0, int t1, const double* __restrict__ etab) {
     const int lane = threadIdx.x & 31;
     const int nchunk = (t1 - t0 + kRows - 1) / kRows;
     const int b = blockIdx.x / nchunk;
@@ -50,12 +51,22 @@ __global__ void __launch_bounds__(32 * kRows) log_softmax_bf16_kernel(const uint
 #pragma unroll
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         double S = 0.0;
+        double lse;
+        if (etab && m >= -700.0f && m <= 700.0f) {  // log Σ exp(x) from the table (no fp64 exp)
 #pragma unroll
-        for (int i = 0; i < kPerLane; ++i)
-            if (lane + 32 * i < Vp1) S += exp((double)v[i] - (double)m);
+            for (int i = 0; i < kPerLane; ++i)
+                if (lane + 32 * i < Vp1) S += __ldg(&etab[__float_as_uint(v[i]) >> 16]);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
-        const double lse = (double)m + log(S);
+            for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+            lse = log(S);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kPerLane; ++i)
+                if (lane + 32 * i < Vp1) S += exp((double)v[i] - (double)m);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+            lse = (double)m + log(S);
+        }
 #pragma unroll
         for (int i = 0; i < kPerLane; ++i) {
             const int w = lane + 32 * i;
@@ -145,7 +156,7 @@ int launch_log_softmax_bf16(const uint16_t* x, int64_t stride_b, int64_t stride_
     if (grid == 0) return 0;
     if (grid > 0x7fffffff) { err = "B * T too large"; return 2; }
     log_softmax_bf16_kernel<<<(int)grid, 32 * kRows, 0, (cudaStream_t)stream>>>(x, stride_b, stride_t, lengths, B, T,
-                                                                                 Vp1, out, t0, t1);
+                                                                                 Vp1, out, t0, t1, bf16_exp_table(stream));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     return 0;

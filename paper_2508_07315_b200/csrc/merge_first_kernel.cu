@@ -154,6 +154,30 @@ __global__ void __launch_bounds__(kNT) merge_first_kernel(const DecodeParams p) 
     auto cut_to_k = [&]() {
         __syncthreads();
         const int n = s_cnt;
+        if (n <= kNT) {
+            // rank selection (the keys are distinct: each group's best member is its own): one
+            // entry per thread, its rank among the n by one pass over the keys, the K best written
+            // to their ranks — two barriers instead of the sorting network's log^2 n / 2
+            uint64_t kk = 0ull;
+            MfPay pp{};
+            int r = kNT;
+            if (tid < n) {
+                kk = s_key[tid];
+                pp = pay[tid];
+                r = 0;
+                for (int j = 0; j < n; ++j) r += s_key[j] > kk ? 1 : 0;
+            }
+            __syncthreads();
+            if (r < K) { s_key[r] = kk; s_idx[r] = r; pay[r] = pp; }
+            __syncthreads();
+            if (tid == 0) {
+                const int keep = min(n, K);
+                s_cnt = keep;
+                if (keep == K) s_tau = fmaxf(s_tau, score_of(s_key[K - 1]));
+            }
+            __syncthreads();
+            return;
+        }
         int n2 = 2;
         while (n2 < n) n2 <<= 1;
         for (int i = n + tid; i < n2; i += kNT) { s_key[i] = 0ull; s_idx[i] = i; }

@@ -447,7 +447,10 @@ def run_flexctc(args):
                     "kernel": "frame_compact_tma_kernel (every valid row once; TMA 2-slot ring per warp, 4-row chunks)",
                     "kernel_ms": 1e3 * cmp_s, "algorithmic_bytes_per_launch": cmp_bytes,
                     "peak_source": peak_src, "traffic_source": ctraffic_src,
-                    "share_of_step": cmp_s / (t_dec / args.steps)}
+                    "share_of_step": cmp_s / (t_dec / args.steps),
+                    "note": ("with LM / boosting the pass also issues the decode's L2 warm-up of the lookup tables "
+                             "(LM level-1 rows and arcs, boost table) between its rows; those prefetched bytes are "
+                             "not counted in algorithmic_bytes_per_launch" if (wl.lm or wl.boost) else None)}
 
     # e2e through the public host-buffer entry (flexctc_decode_host): H2D + decode + D2H per step
     e2e = None

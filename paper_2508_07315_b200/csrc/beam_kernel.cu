@@ -1648,63 +1648,68 @@ int launch_decode(const DecodeParams& p, void* stream, void* ev0, void* ev1, std
         e = cudaGetLastError();
         if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
     }
-    const char* e_w = getenv("FLEXCTC_L2_WARM");  // "0": no warm-up (A/B switch)
-    if ((p.use_lm || p.use_bt) && !(e_w && e_w[0] == '0') && !plain) {
-        int dev = 0, nsm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        const char* e_wr = getenv("FLEXCTC_L2_WARM_REC");  // "1": also the LM state records (A/B)
-        const bool warm_rec = e_wr && e_wr[0] == '1';
-        l2_warm_kernel<<<4 * nsm, 256, 0, st>>>((const char*)p.lm.dense, p.use_lm ? p.lm.dense_bytes : 0,
-                                                (const char*)p.lm.arcs, p.use_lm ? p.lm.arcs_bytes : 0,
-                                                (const char*)p.bt.tab, p.use_bt ? p.bt.tab_bytes : 0,
-                                                (const char*)p.lm.rec, p.use_lm && warm_rec ? p.lm.rec_bytes : 0);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
-    }
-    if (p.merge_first) return launch_merge_first(p, stream, ev0, ev1, err);  // reading R27
-    if (greedy) return launch_greedy(p, stream, ev0, ev1, err);
-    if (use_warp_path(p)) {
-        // K <= 32: the bandwidth-bound compaction pass over every valid row, then one warp per
-        // utterance (warp_beam_kernel.cu)
-        int rc = launch_rowoff(p.len_c, p.B, p.rowoff, stream, err);
-        if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev2, st);
-        if (!rc) rc = launch_compact(p.logits ? (const void*)p.logits : (const void*)p.log_probs, p.logits != nullptr,
-                                     p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err);
-        if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev3, st);
-        if (!rc) rc = launch_warp_beam(p, p.logits != nullptr, stream, ev0, ev1, err);
-        return rc;
-    }
-    const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
-    // The persistent CTA kernel reads the frame records of the compaction pass (the best token, the
-    // listed band and its floor) instead of computing per-frame summaries from the rows when the
-    // log-probs are resident and the decode has the north-star shape at B <= #SMs (beam 16,
-    // V' = 1025, 4-gram LM + boosting: its specialised variant reads records, and with the
+    // which kernels run: merge-first, greedy, the warp path, or the CTA kernel (with or without the
+    // compaction records). The CTA kernel reads the frame records of the compaction pass (the best
+    // token, the listed band and its floor) instead of computing per-frame summaries from the rows
+    // when the log-probs are resident and the decode has the north-star shape at B <= #SMs (beam
+    // 16, V' = 1025, 4-gram LM + boosting: its specialised variant reads records, and with the
     // settled-beam fast path the helper warps' summaries are on the critical path: c4 1.542 ->
     // 1.535 ms per decode including the pass, profiles/r2/ab_records_fastpath.jsonl). Elsewhere the
     // pass costs more than it saves (c5 5.873 -> 5.961 ms, profiles/r2/cta_records_ab.jsonl).
     // FLEXCTC_CMP=0 / 1 forces it off / on (A/B and test switch).
+    const bool warp = !p.merge_first && !greedy && use_warp_path(p);
     DecodeParams q = p;
-    const char* e_cmp = getenv("FLEXCTC_CMP");
-    bool want_cmp = false;
-    {
+    if (!p.merge_first && !greedy && !warp) {
+        const char* e_cmp = getenv("FLEXCTC_CMP");
         int dev = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        want_cmp = p.K == 16 && p.Vp1 == 1025 && p.use_lm && p.lm.RW == 16 && p.use_bt && p.merge_mode == 0 &&
-                   !p.retract && p.alpha_lm >= 0.0f && p.alpha_bt >= 0.0f && !p.fuse_rep && p.B <= nsm;
+        bool want_cmp = p.K == 16 && p.Vp1 == 1025 && p.use_lm && p.lm.RW == 16 && p.use_bt && p.merge_mode == 0 &&
+                        !p.retract && p.alpha_lm >= 0.0f && p.alpha_bt >= 0.0f && !p.fuse_rep && p.B <= nsm;
+        if (e_cmp) want_cmp = e_cmp[0] == '1';
+        q.use_cmp = p.cmp && p.rowoff && !p.ready && (!p.logits || cta_logits_direct(p)) && want_cmp ? 1 : 0;
+        if (p.logits && !q.use_cmp) { err = "bf16 logits: the CTA kernel reads them only with records"; return 2; }
     }
-    if (e_cmp) want_cmp = e_cmp[0] == '1';
-    q.use_cmp = p.cmp && p.rowoff && !p.ready && (!p.logits || cta_logits_direct(p)) && want_cmp ? 1 : 0;
-    if (p.logits && !q.use_cmp) { err = "bf16 logits: the CTA kernel reads them only with records"; return 2; }
-    if (q.use_cmp) {
+    const bool compacts = warp || q.use_cmp;
+
+    // L2 warm-up of the fusion tables the frame loop looks up at random: interleaved with the
+    // compaction pass's rows when the decode runs one (no separate launch), else its own launch
+    const char* e_w = getenv("FLEXCTC_L2_WARM");  // "0": no warm-up (A/B switch)
+    WarmRanges wr;
+    bool warm_in_pass = false;
+    if ((p.use_lm || p.use_bt) && !(e_w && e_w[0] == '0') && !plain) {
+        const char* e_wr = getenv("FLEXCTC_L2_WARM_REC");  // "1": also the LM state records (A/B)
+        const bool warm_rec = e_wr && e_wr[0] == '1';
+        wr.a[0] = (const char*)p.lm.dense; wr.n[0] = p.use_lm ? p.lm.dense_bytes : 0;
+        wr.a[1] = (const char*)p.lm.arcs;  wr.n[1] = p.use_lm ? p.lm.arcs_bytes : 0;
+        wr.a[2] = (const char*)p.bt.tab;   wr.n[2] = p.use_bt ? p.bt.tab_bytes : 0;
+        wr.a[3] = (const char*)p.lm.rec;   wr.n[3] = p.use_lm && warm_rec ? p.lm.rec_bytes : 0;
+        const char* e_wf = getenv("FLEXCTC_WARM_IN_PASS");  // "0": separate launch (A/B switch)
+        warm_in_pass = compacts && compact_fuses_warm(p.Vp1, p.logits != nullptr) && !(e_wf && e_wf[0] == '0');
+        if (!warm_in_pass) {
+            int dev = 0, nsm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            l2_warm_kernel<<<4 * nsm, 256, 0, st>>>(wr.a[0], wr.n[0], wr.a[1], wr.n[1], wr.a[2], wr.n[2], wr.a[3], wr.n[3]);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) { err = cudaGetErrorString(e); return 1; }
+        }
+    }
+    if (p.merge_first) return launch_merge_first(p, stream, ev0, ev1, err);  // reading R27
+    if (greedy) return launch_greedy(p, stream, ev0, ev1, err);
+    if (compacts) {
+        // the bandwidth-bound compaction pass over every valid row, then the warp kernel (K <= 32,
+        // one warp per utterance, warp_beam_kernel.cu) or the CTA kernel reading the records
         int rc = launch_rowoff(p.len_c, p.B, p.rowoff, stream, err);
         if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev2, st);
         if (!rc) rc = launch_compact(p.logits ? (const void*)p.logits : (const void*)p.log_probs, p.logits != nullptr,
-                                     p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err);
+                                     p.stride_b, p.stride_t, p.rowoff, p.B, p.T, p.Vp1, p.cmp, stream, err,
+                                     warm_in_pass ? &wr : nullptr);
         if (!rc && ev2 && ev3) cudaEventRecord((cudaEvent_t)ev3, st);
         if (rc) return rc;
+        if (warp) return launch_warp_beam(p, p.logits != nullptr, stream, ev0, ev1, err);
     }
+    const bool small_lm = !p.use_lm || p.lm.NL <= 2;  // order <= 4: two arc levels
     return small_lm ? launch_lmv<2>(q, st, ev0, ev1, err) : launch_lmv<kMaxLmLevels>(q, st, ev0, ev1, err);
 }
 

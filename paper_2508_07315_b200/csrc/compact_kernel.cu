@@ -474,7 +474,7 @@ template <bool BF16, int kStages>
 __global__ void __launch_bounds__(32 * kTWarps, kStages == 2 && !BF16 ? 3 : 2)
     frame_compact_tma_kernel(const void* __restrict__ X, int64_t sb, int64_t stt, const int64_t* __restrict__ rowoff,
                              int B, int T, int Vp1, uint8_t* __restrict__ cmp, const char* lo, const char* hi,
-                             int sbytes, const double* __restrict__ etab) {
+                             int sbytes, const double* __restrict__ etab, const WarmRanges warm) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const size_t esz = BF16 ? 2 : 4;
@@ -516,9 +516,25 @@ __global__ void __launch_bounds__(32 * kTWarps, kStages == 2 && !BF16 ? 3 : 2)
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s)
         if (row_of(s) < nrows) issue(s, s);
+    // L2 warm-up of the decode's lookup tables, interleaved with the rows: at row k every thread
+    // prefetches line gtid + k * nthreads of the concatenated ranges (evict-last)
+    const int64_t wl0 = (warm.n[0] + 127) >> 7, wl1 = (warm.n[1] + 127) >> 7, wl2 = (warm.n[2] + 127) >> 7,
+                  wl3 = (warm.n[3] + 127) >> 7;
+    const int64_t wlines = wl0 + wl1 + wl2 + wl3;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gthreads = (int64_t)gridDim.x * blockDim.x;
+    auto warm_step = [&](int k) {
+        const int64_t i = gtid + (int64_t)k * gthreads;
+        if (i >= wlines) return;
+        const char* q = i < wl0 ? warm.a[0] + (i << 7)
+                        : i < wl0 + wl1 ? warm.a[1] + ((i - wl0) << 7)
+                        : i < wl0 + wl1 + wl2 ? warm.a[2] + ((i - wl0 - wl1) << 7) : warm.a[3] + ((i - wl0 - wl1 - wl2) << 7);
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(q));
+    };
     uint32_t ph = 0;
     int s = 0;
-    for (int k = 0; row_of(k) < nrows; ++k) {
+    int k = 0;
+    for (; row_of(k) < nrows; ++k) {
+        warm_step(k);
         const int kn = k + kStages - 1;
         const int sn = s == 0 ? kStages - 1 : s - 1;  // the slot ranked in the previous iteration
         if (row_of(kn) < nrows) issue(kn, sn);
@@ -531,6 +547,7 @@ __global__ void __launch_bounds__(32 * kTWarps, kStages == 2 && !BF16 ? 3 : 2)
         __syncwarp();  // the slot and the key buffer are free again
         s = s + 1 == kStages ? 0 : s + 1;
     }
+    for (; gtid + (int64_t)k * gthreads < wlines; ++k) warm_step(k);  // lines left after the rows
 }
 
 // rowoff[b] = Σ_{b' < b} len_c[b'], rowoff[B] = Σ L (one CTA; block scan over 1024-wide tiles)
@@ -613,8 +630,16 @@ int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, st
 // rowoff [B + 1] (launch_rowoff) on the device. Rows that fit the registers: the TMA-staged pass,
 // a persistent grid of #SMs x its occupancy; longer rows: the register-loading kernel, one warp per
 // 4 rows, grid = #SMs x 16 CTAs at most (grid stride over Σ L_b / 4 row chunks).
+bool compact_fuses_warm(int Vp1, bool bf16) {
+    const char* e = getenv("FLEXCTC_CMP_TMA");
+    if (e && e[0] == '0') return false;
+    const int esz = bf16 ? 2 : 4, epb = bf16 ? 8 : 4;
+    const int nblk_max = ((16 - esz) / esz + Vp1 + epb - 1) / epb;
+    return nblk_max <= 32 * (bf16 ? kBlk<true> : kBlk<false>);
+}
+
 int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t, const int64_t* rowoff, int B, int T,
-                   int Vp1, uint8_t* cmp, void* stream, std::string& err) {
+                   int Vp1, uint8_t* cmp, void* stream, std::string& err, const WarmRanges* warm) {
     if (B == 0 || T == 0) return 0;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
@@ -640,7 +665,8 @@ int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t,
         const int64_t want = ((int64_t)B * T + kTWarps * kTChunk - 1) / (kTWarps * kTChunk);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(occ, 1)));
         const double* etab = bf16 ? bf16_exp_table(st) : nullptr;  // NULL: the pass evaluates exp itself
-        kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes, etab);
+        kern<<<grid, 32 * kTWarps, smem, st>>>(x, stride_b, stride_t, rowoff, B, T, Vp1, cmp, lo, hi, sbytes, etab,
+                                               warm ? *warm : WarmRanges{});
     } else {
         const int64_t max_chunks = ((int64_t)B * T + kRowsPerWarp - 1) / kRowsPerWarp;
         const int64_t want = (max_chunks + kWarps - 1) / kWarps;

@@ -173,8 +173,17 @@ int launch_rowoff(const int32_t* len_c, int B, int64_t* rowoff, void* stream, st
 // exp(x) in fp64 for every bf16 bit pattern x (65536 entries, one per device, built on first use;
 // NULL if it cannot be allocated): the log-sum-exp of bf16 rows by table loads (reading R25)
 const double* bf16_exp_table(void* stream);
+// byte ranges the decode's lookups hit at random (LM level-1 rows and arcs, boost table, ...),
+// prefetched into L2 with evict-last priority
+struct WarmRanges {
+    const char* a[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t n[4] = {0, 0, 0, 0};
+};
+// warm (optional): the TMA pass interleaves the L2 warm-up of these ranges with its rows (no
+// separate l2_warm launch); compact_fuses_warm tells whether the pass will take them
 int launch_compact(const void* x, bool bf16, int64_t stride_b, int64_t stride_t, const int64_t* rowoff, int B, int T,
-                   int Vp1, uint8_t* cmp, void* stream, std::string& err);
+                   int Vp1, uint8_t* cmp, void* stream, std::string& err, const WarmRanges* warm = nullptr);
+bool compact_fuses_warm(int Vp1, bool bf16);
 // warp-per-utterance beam kernel (warp_beam_kernel.cu), K <= 32, after launch_compact
 int launch_warp_beam(const DecodeParams& p, bool bf16, void* stream, void* ev_start, void* ev_stop, std::string& err);
 size_t warp_beam_smem_per_warp(int Vp1, bool bf16, int nch);

@@ -8,7 +8,6 @@ mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 timeout 1800 python -m pytest tests -q -m gpu > $O/pytest.log 2>&1
 python bench.py > $O/bench_c4.log 2>&1
-FLEXCTC_OVERLAP=0 python bench.py --no-cpu-baseline --no-e2e > $O/bench_c4_serial.log 2>&1
 python bench.py --input bf16-logits > $O/bench_c4_bf16.log 2>&1
 python bench.py --workload c5 --steps 20 > $O/bench_c5.log 2>&1
 FLEXCTC_CMP=1 python bench.py --workload c5 --no-cpu-baseline --no-e2e --steps 10 > $O/bench_c5_records.log 2>&1
@@ -27,7 +26,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file
 ncu --set full --clock-control none --import-source on -k regex:ctc_beam -s 3 -c 1 -o $O/prof_beam_c4 \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:frame_compact -s 3 -c 1 -o $O/prof_compact_c4 \
-    env FLEXCTC_OVERLAP=0 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:frame_compact -s 3 -c 1 -o $O/prof_compact_c5 \
     env FLEXCTC_CMP=1 python bench.py --workload c5 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 (echo "## memcheck"; compute-sanitizer --tool memcheck python tests/sanitize_run.py 2>&1 | tail -25;

@@ -1071,11 +1071,15 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     // dead slots need no backpointer: the backtrace only follows live ancestors
                 }
             }
-            gsync(G);
+            // the live slots are a prefix of the (score desc) selection; count them with the barrier
+            int nlive_all = 0;
+            if (G == 32) gsync(G); else nlive_all = __syncthreads_count(live ? 1 : 0);
             const long long c6 = TCLK();
             // ------------------------------------------------ phase 7: RecombineHypotheses
             unsigned grp = 0;
-            const bool small_beam = K <= 32;  // all slots live in warp 0
+            // all live slots in warp 0: K <= 32, or (K > 32) at most 32 of them live this frame (the
+            // common case at c5), where match.any replaces the shared hash table
+            const bool small_beam = K <= 32 || (G != 32 && nlive_all <= 32);
             if (small_beam && tid < 32) {
                 // one warp holds the beam: group lanes by (hash, last) with match.any
                 const bool lv = tid < K && my_acc > kNeg;

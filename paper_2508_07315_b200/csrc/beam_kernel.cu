@@ -918,15 +918,22 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     // parallel evaluation of the batch (one round of LM arc searches for up to
                     // kPairCap pairs). A lane whose pair list is full records where it stopped and
                     // resumes after the batch (no pair is collected twice).
-                    for (int base = 0; base < m; base += G4) {
-                        const int j = base + tid;
-                        const int w = j < m ? (int)sm.toks[j] : -1;
+                    // With few listed tokens, LT = 2..8 threads share a token, each taking every
+                    // LT-th live slot from its own offset (shorter serial chains; the early exit
+                    // stays valid per thread: the suffix maxima cover every later slot).
+                    int lt_sh = 0;
+                    while (lt_sh < 3 && (m << (lt_sh + 1)) <= G4) ++lt_sh;
+                    const int LT = 1 << lt_sh;
+                    for (int base = 0; base < (m << lt_sh); base += G4) {
+                        const int jj = base + tid;
+                        const int j = jj >> lt_sh;
+                        const int w = jj < (m << lt_sh) ? (int)sm.toks[j] : -1;
                         const float dw = w >= 0 ? row[w] : 0.0f;
-                        int a_from = w >= 0 ? 0 : nalive;
+                        int a_from = w >= 0 ? (jj & (LT - 1)) : nalive;
                         for (;;) {
                             const float thr = sc.thr;
                             bool full = false;
-                            for (int a2 = a_from; a2 < nalive; ++a2) {
+                            for (int a2 = a_from; a2 < nalive; a2 += LT) {
                                 {   // no later live slot can reach thr with this token: stop
                                     const float2 sf = s_suf[a2];
                                     const float reach = __fadd_rn(__fadd_rn(sf.x, dw), ubvmax);

@@ -918,11 +918,11 @@ __global__ void __launch_bounds__(NT, 1) ctc_beam_kernel(const DecodeParams p, c
                     // parallel evaluation of the batch (one round of LM arc searches for up to
                     // kPairCap pairs). A lane whose pair list is full records where it stopped and
                     // resumes after the batch (no pair is collected twice).
-                    // With few listed tokens, LT = 2..8 threads share a token, each taking every
+                    // With few listed tokens, LT = 2..32 threads share a token, each taking every
                     // LT-th live slot from its own offset (shorter serial chains; the early exit
                     // stays valid per thread: the suffix maxima cover every later slot).
                     int lt_sh = 0;
-                    while (lt_sh < 3 && (m << (lt_sh + 1)) <= G4) ++lt_sh;
+                    while (lt_sh < 5 && (m << (lt_sh + 1)) <= G4) ++lt_sh;
                     const int LT = 1 << lt_sh;
                     for (int base = 0; base < (m << lt_sh); base += G4) {
                         const int jj = base + tid;
